@@ -1,0 +1,821 @@
+// Host runtime and C ABI (include/ibm.h) of the B200 IBM hot path.
+//
+// One process per GPU.  The grid is split into slabs along y:
+// with NCCL (nranks > 1) each process owns one slab and exchanges 2-row halos
+// with grouped ncclSend/ncclRecv and the SOR residual with ncclAllReduce(max on
+// the uint64 bit pattern, exact); in loopback mode (test) all slabs live in one
+// ctx and the same exchanges are device-to-device copies.  Everything stays in
+// HBM; per step only the SOR control words and 4 force sums reach the host.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include <nccl.h>
+
+#include "ibm_internal.h"
+
+using namespace ibm;
+
+struct ibm_ctx : public Ctx {};
+
+namespace {
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess) {                                                              \
+      c.err = std::string(#call) + ": " + cudaGetErrorString(e_);                         \
+      return IBM_ERR_CUDA;                                                                \
+    }                                                                                     \
+  } while (0)
+
+#define NK(call)                                                                          \
+  do {                                                                                    \
+    ncclResult_t r_ = (call);                                                             \
+    if (r_ != ncclSuccess) {                                                              \
+      c.err = std::string(#call) + ": " + ncclGetErrorString(r_);                         \
+      return IBM_ERR_NCCL;                                                                \
+    }                                                                                     \
+  } while (0)
+
+long round_up(long x, long a) { return (x + a - 1) / a * a; }
+
+struct Carver {
+  char *base;
+  size_t off;
+  template <class T>
+  T *take(size_t n) {
+    size_t a = (off + 255) & ~size_t(255);
+    off = a + n * sizeof(T);
+    return base ? reinterpret_cast<T *>(base + a) : nullptr;
+  }
+};
+
+int check_config(const ibm_config *cfg, std::string &why) {
+  if (!cfg) { why = "cfg is NULL"; return IBM_ERR_ARG; }
+  if (cfg->nx < 4 || cfg->ny < 4) { why = "nx, ny must be >= 4"; return IBM_ERR_CONFIG; }
+  if (!cfg->xn || !cfg->yn) { why = "xn/yn NULL"; return IBM_ERR_ARG; }
+  for (int i = 0; i < cfg->nx; ++i)
+    if (!(cfg->xn[i + 1] > cfg->xn[i])) { why = "xn not strictly increasing"; return IBM_ERR_CONFIG; }
+  for (int j = 0; j < cfg->ny; ++j)
+    if (!(cfg->yn[j + 1] > cfg->yn[j])) { why = "yn not strictly increasing"; return IBM_ERR_CONFIG; }
+  if (!(cfg->Re > 0)) { why = "Re <= 0"; return IBM_ERR_CONFIG; }
+  if (!(cfg->dt > 0)) { why = "dt <= 0"; return IBM_ERR_CONFIG; }
+  if (!(cfg->omega_p >= 1.0 && cfg->omega_p < 2.0)) { why = "omega_p outside [1,2)"; return IBM_ERR_CONFIG; }
+  if (!(cfg->omega_uv >= 1.0 && cfg->omega_uv < 2.0)) { why = "omega_uv outside [1,2)"; return IBM_ERR_CONFIG; }
+  if (!(cfg->tol_p > 0) || !(cfg->tol_uv > 0)) { why = "tolerances must be > 0"; return IBM_ERR_CONFIG; }
+  if (cfg->maxit_p < 1 || cfg->maxit_uv < 1) { why = "maxit must be >= 1"; return IBM_ERR_CONFIG; }
+  if (cfg->nranks < 1 || (!cfg->loopback && (cfg->rank < 0 || cfg->rank >= cfg->nranks))) {
+    why = "rank/nranks inconsistent";
+    return IBM_ERR_CONFIG;
+  }
+  if (cfg->ny / cfg->nranks < 4) { why = "slabs need >= 4 rows"; return IBM_ERR_CONFIG; }
+  if (cfg->nranks > 1 && !cfg->loopback && !cfg->nccl_id) { why = "nccl_id required for nranks > 1"; return IBM_ERR_CONFIG; }
+  return IBM_OK;
+}
+
+void slab_rows(int ny, int P, int r, int *j0, int *j1) {
+  int base = ny / P, rem = ny % P;
+  *j0 = r * base + (r < rem ? r : rem);
+  *j1 = *j0 + base + (r < rem ? 1 : 0);
+}
+
+Slab make_slab(const ibm_config &cfg, int r) {
+  Slab s;
+  std::memset(&s, 0, sizeof(s));
+  s.rank = r;
+  slab_rows(cfg.ny, cfg.nranks, r, &s.pj0, &s.pj1);
+  const int nj = s.pj1 - s.pj0;
+  const bool last = (r == cfg.nranks - 1);
+  s.gu = Geo{cfg.nx + 1, nj, s.pj0, cfg.ny, round_up(cfg.nx + 1, 32)};
+  s.gv = Geo{cfg.nx, nj + (last ? 1 : 0), s.pj0, cfg.ny + 1, round_up(cfg.nx, 32)};
+  s.gp = Geo{cfg.nx, nj, s.pj0, cfg.ny, round_up(cfg.nx, 32)};
+  s.bu = s.bv = s.bpb = BBox{0, 0, 0, 0};
+  return s;
+}
+
+size_t rho_len(const ibm_config &cfg) {
+  int m = cfg.maxit_p > cfg.maxit_uv ? cfg.maxit_p : cfg.maxit_uv;
+  return (size_t)m + 2;
+}
+
+// carves everything; base == nullptr -> size only
+size_t carve(Ctx &c, char *base) {
+  Carver cv{base, 0};
+  const int nx = c.cfg.nx, ny = c.cfg.ny;
+  Metric &m = c.m;
+  m.xn = cv.take<double>(nx + 1); m.yn = cv.take<double>(ny + 1);
+  m.dx = cv.take<double>(nx); m.dy = cv.take<double>(ny);
+  m.xc = cv.take<double>(nx); m.yc = cv.take<double>(ny);
+  m.hxc = cv.take<double>(nx); m.hyc = cv.take<double>(ny);
+  m.cEu = cv.take<double>(nx + 1); m.cWu = cv.take<double>(nx + 1); m.cDu = cv.take<double>(nx + 1);
+  m.cNu = cv.take<double>(ny); m.cSu = cv.take<double>(ny);
+  m.cEv = cv.take<double>(nx); m.cWv = cv.take<double>(nx); m.cDv = cv.take<double>(nx);
+  m.cNv = cv.take<double>(ny + 1); m.cSv = cv.take<double>(ny + 1);
+  m.cEp = cv.take<double>(nx); m.cWp = cv.take<double>(nx); m.cDp = cv.take<double>(nx);
+  m.cNp = cv.take<double>(ny); m.cSp = cv.take<double>(ny);
+  c.rho_bits = cv.take<unsigned long long>(rho_len(c.cfg));
+  c.ctl = cv.take<SorCtl>(1);
+  c.nanflag = cv.take<int>(4);
+  for (Slab &s : c.sl) {
+    const size_t nu = s.gu.elems(), nv = s.gv.elems(), np = s.gp.elems();
+    s.u = cv.take<double>(nu); s.cu = cv.take<double>(nu); s.cup = cv.take<double>(nu);
+    s.us[0] = cv.take<double>(nu); s.us[1] = cv.take<double>(nu); s.ru = cv.take<double>(nu);
+    s.fu = cv.take<double>(nu);
+    s.v = cv.take<double>(nv); s.cv = cv.take<double>(nv); s.cvp = cv.take<double>(nv);
+    s.vs[0] = cv.take<double>(nv); s.vs[1] = cv.take<double>(nv); s.rv = cv.take<double>(nv);
+    s.fv = cv.take<double>(nv);
+    s.p = cv.take<double>(np); s.phi[0] = cv.take<double>(np); s.phi[1] = cv.take<double>(np);
+    s.bp = cv.take<double>(np); s.q = cv.take<double>(np);
+    s.tu = cv.take<uint8_t>(nu); s.tv = cv.take<uint8_t>(nv); s.tp = cv.take<uint8_t>(np);
+    s.pf = cv.take<uint8_t>(np);
+    s.red = cv.take<double>(4);
+  }
+  return cv.off + 256;
+}
+
+// Host metric arrays: the same formulas as the oracle's, evaluated
+// in IEEE double on the host (compiled with -ffp-contract=off).
+struct HostMetric {
+  std::vector<double> xn, yn, dx, dy, xc, yc, hxc, hyc;
+  std::vector<double> cEu, cWu, cDu, cNu, cSu, cEv, cWv, cDv, cNv, cSv, cEp, cWp, cDp, cNp, cSp;
+};
+
+HostMetric host_metric(const ibm_config &cfg) {
+  const int nx = cfg.nx, ny = cfg.ny;
+  HostMetric h;
+  h.xn.assign(cfg.xn, cfg.xn + nx + 1);
+  h.yn.assign(cfg.yn, cfg.yn + ny + 1);
+  h.dx.resize(nx); h.xc.resize(nx); h.hxc.assign(nx, 0.0);
+  h.dy.resize(ny); h.yc.resize(ny); h.hyc.assign(ny, 0.0);
+  for (int i = 0; i < nx; ++i) { h.dx[i] = h.xn[i + 1] - h.xn[i]; h.xc[i] = 0.5 * (h.xn[i] + h.xn[i + 1]); }
+  for (int j = 0; j < ny; ++j) { h.dy[j] = h.yn[j + 1] - h.yn[j]; h.yc[j] = 0.5 * (h.yn[j] + h.yn[j + 1]); }
+  for (int i = 1; i < nx; ++i) h.hxc[i] = h.xc[i] - h.xc[i - 1];
+  for (int j = 1; j < ny; ++j) h.hyc[j] = h.yc[j] - h.yc[j - 1];
+  const auto &dx = h.dx, &dy = h.dy, &hxc = h.hxc, &hyc = h.hyc;
+  // u family (interior 1 <= i <= nx-1): zero-gradient outlet, slip walls
+  h.cEu.assign(nx + 1, 0.0); h.cWu.assign(nx + 1, 0.0); h.cDu.assign(nx + 1, 0.0);
+  h.cNu.assign(ny, 0.0); h.cSu.assign(ny, 0.0);
+  for (int i = 1; i <= nx - 1; ++i) {
+    if (i <= nx - 2) h.cEu[i] = 1.0 / (hxc[i] * dx[i]);
+    h.cWu[i] = 1.0 / (hxc[i] * dx[i - 1]);
+  }
+  for (int j = 0; j < ny; ++j) {
+    if (j <= ny - 2) h.cNu[j] = 1.0 / (dy[j] * hyc[j + 1]);
+    if (j >= 1) h.cSu[j] = 1.0 / (dy[j] * hyc[j]);
+  }
+  // v family (interior 1 <= j <= ny-1): Dirichlet v = 0 on the inlet face, zero-gradient outlet
+  h.cEv.assign(nx, 0.0); h.cWv.assign(nx, 0.0); h.cDv.assign(nx, 0.0);
+  h.cNv.assign(ny + 1, 0.0); h.cSv.assign(ny + 1, 0.0);
+  for (int i = 0; i < nx; ++i) {
+    if (i <= nx - 2) h.cEv[i] = 1.0 / (dx[i] * hxc[i + 1]);
+    if (i >= 1) h.cWv[i] = 1.0 / (dx[i] * hxc[i]);
+  }
+  h.cDv[0] = 2.0 / (dx[0] * dx[0]);
+  for (int j = 1; j <= ny - 1; ++j) {
+    h.cNv[j] = 1.0 / (hyc[j] * dy[j]);
+    h.cSv[j] = 1.0 / (hyc[j] * dy[j - 1]);
+  }
+  // p / phi: Neumann inlet and walls, phi = 0 on the outlet face
+  h.cEp.assign(nx, 0.0); h.cWp.assign(nx, 0.0); h.cDp.assign(nx, 0.0);
+  h.cNp.assign(ny, 0.0); h.cSp.assign(ny, 0.0);
+  for (int i = 0; i < nx; ++i) {
+    if (i <= nx - 2) h.cEp[i] = 1.0 / (dx[i] * hxc[i + 1]);
+    if (i >= 1) h.cWp[i] = 1.0 / (dx[i] * hxc[i]);
+  }
+  h.cDp[nx - 1] = 2.0 / (dx[nx - 1] * dx[nx - 1]);
+  for (int j = 0; j < ny; ++j) {
+    if (j <= ny - 2) h.cNp[j] = 1.0 / (dy[j] * hyc[j + 1]);
+    if (j >= 1) h.cSp[j] = 1.0 / (dy[j] * hyc[j]);
+  }
+  return h;
+}
+
+// Eqs. (1)-(2), on the host (same libm as the oracle)
+void plunge(double t, double hbar, double k, double *y, double *yd) {
+  *y = hbar * sin(k * t);
+  *yd = (k * hbar) * cos(k * t);
+}
+
+BBox box_for(const std::vector<double> &xs, const std::vector<double> &ys, double xlo, double xhi, double ylo,
+             double yhi, const Geo &g, int margin) {
+  const int ni = (int)xs.size(), NJ = (int)ys.size();
+  int i0 = 0, i1 = ni, j0 = 0, j1 = NJ;
+  while (i0 < ni && xs[i0] < xlo) ++i0;
+  while (i1 > 0 && xs[i1 - 1] > xhi) --i1;
+  while (j0 < NJ && ys[j0] < ylo) ++j0;
+  while (j1 > 0 && ys[j1 - 1] > yhi) --j1;
+  if (i1 < i0) i1 = i0;
+  if (j1 < j0) j1 = j0;
+  i0 = std::max(0, i0 - margin); i1 = std::min(ni, i1 + margin);
+  j0 = std::max(0, j0 - margin); j1 = std::min(NJ, j1 + margin);
+  BBox b{i0, i1, j0 - g.gj0, j1 - g.gj0};
+  b.j0 = std::max(b.j0, -kGhost);
+  b.j1 = std::min(b.j1, g.nj + kGhost);
+  if (b.j1 < b.j0) b.j1 = b.j0;
+  return b;
+}
+
+// ---------------------------------------------------------------- halos and reductions
+// exchange 2 ghost rows of one family buffer (selected per slab by `pick`)
+template <class Pick>
+int halo(Ctx &c, Pick pick) {
+  const size_t esz = sizeof(double);
+  if (c.loopback) {
+    for (size_t r = 0; r + 1 < c.sl.size(); ++r) {
+      double *lo, *up;
+      const Geo *glo, *gup;
+      pick(c.sl[r], &lo, &glo);
+      pick(c.sl[r + 1], &up, &gup);
+      const size_t bytes = (size_t)kGhost * glo->pitch * esz;
+      CK(cudaMemcpyAsync(up + gup->off(0, -kGhost), lo + glo->off(0, glo->nj - kGhost), bytes,
+                         cudaMemcpyDeviceToDevice, c.stream));
+      CK(cudaMemcpyAsync(lo + glo->off(0, glo->nj), up + gup->off(0, 0), bytes, cudaMemcpyDeviceToDevice,
+                         c.stream));
+    }
+    return IBM_OK;
+  }
+  if (c.nranks == 1) return IBM_OK;
+  ncclComm_t comm = (ncclComm_t)c.nccl;
+  double *buf;
+  const Geo *g;
+  pick(c.sl[0], &buf, &g);
+  const int r = c.sl[0].rank;
+  const size_t cnt = (size_t)kGhost * g->pitch;
+  NK(ncclGroupStart());
+  if (r > 0) {
+    NK(ncclSend(buf + g->off(0, 0), cnt, ncclFloat64, r - 1, comm, c.stream));
+    NK(ncclRecv(buf + g->off(0, -kGhost), cnt, ncclFloat64, r - 1, comm, c.stream));
+  }
+  if (r < c.nranks - 1) {
+    NK(ncclSend(buf + g->off(0, g->nj - kGhost), cnt, ncclFloat64, r + 1, comm, c.stream));
+    NK(ncclRecv(buf + g->off(0, g->nj), cnt, ncclFloat64, r + 1, comm, c.stream));
+  }
+  NK(ncclGroupEnd());
+  return IBM_OK;
+}
+
+#define HALO(expr)                                                            \
+  do {                                                                        \
+    int st_ = halo(c, [&](Slab &s, double **b, const Geo **g) { expr; });     \
+    if (st_) return st_;                                                      \
+  } while (0)
+
+bool multi(const Ctx &c) { return c.sl.size() > 1 || c.nranks > 1; }
+
+// Sums of the 4 force partials over slabs (loopback: host, in slab order) or
+// ranks (NCCL sum all-reduce, in place, before the copy).
+int force_sums(Ctx &c, double out[4]) {
+  if (!c.loopback && c.nranks > 1) {
+    NK(ncclAllReduce(c.sl[0].red, c.sl[0].red, 4, ncclFloat64, ncclSum, (ncclComm_t)c.nccl, c.stream));
+    NK(ncclAllReduce(c.nanflag, c.nanflag, 1, ncclInt32, ncclMax, (ncclComm_t)c.nccl, c.stream));
+  }
+  for (size_t r = 0; r < c.sl.size(); ++r)
+    CK(cudaMemcpyAsync(c.h_red + 4 * r, c.sl[r].red, 4 * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaMemcpyAsync(c.h_nan, c.nanflag, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  for (int q = 0; q < 4; ++q) out[q] = 0.0;
+  for (size_t r = 0; r < c.sl.size(); ++r)
+    for (int q = 0; q < 4; ++q) out[q] = out[q] + c.h_red[4 * r + q];
+  return IBM_OK;
+}
+
+// solid momentum M at the current tags and fields (R20)
+int refresh_time(Ctx &c) {
+  const double t = (double)c.step * c.cfg.dt;
+  double yb = c.body.y0, vb = 0.0, disp = 0.0;
+  if (c.body.has) {
+    plunge(t, c.body.hbar, c.body.k, &disp, &vb);
+    yb = c.body.y0 + disp;
+    for (Slab &s : c.sl) launch_classify(c, s, yb);
+  }
+  for (Slab &s : c.sl) launch_forces(c, s);
+  CK(cudaGetLastError());
+  double sums[4];
+  int st = force_sums(c, sums);
+  if (st) return st;
+  c.Mx = sums[1];
+  c.My = sums[3];
+  return IBM_OK;
+}
+
+// ---------------------------------------------------------------- SOR driver
+// Launches iterations in batches; each iteration kernel early-exits once the
+// device control block says converged, so the host polls once per batch.
+int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *status, int iters_override) {
+  const ibm_config &cfg = c.cfg;
+  const int maxit = iters_override > 0 ? iters_override : (helm ? cfg.maxit_uv : cfg.maxit_p);
+  const double tol = iters_override > 0 ? -1.0 : (helm ? cfg.tol_uv : cfg.tol_p);
+  const double omega = helm ? cfg.omega_uv : cfg.omega_p;
+  CK(cudaMemsetAsync(c.rho_bits, 0, sizeof(unsigned long long) * (size_t)(maxit + 2), c.stream));
+  c.h_ctl[1] = SorCtl{0ull, -1, 0, 0u, 0};
+  CK(cudaMemcpyAsync(c.ctl, &c.h_ctl[1], sizeof(SorCtl), cudaMemcpyHostToDevice, c.stream));
+  const bool mult = multi(c);
+  std::vector<SorArgs> args(c.sl.size());
+  std::vector<int> grids(c.sl.size());
+  for (size_t r = 0; r < c.sl.size(); ++r) {
+    Slab &s = c.sl[r];
+    SorArgs &a = args[r];
+    std::memset(&a, 0, sizeof(a));
+    a.helmholtz = helm ? 1 : 0;
+    a.beta = cfg.dt * (0.5 / cfg.Re);
+    a.omega = omega;
+    a.omc = 1.0 - omega;
+    a.tol = tol;
+    a.maxit = maxit;
+    a.check_every = cfg.check_every;
+    a.rho_bits = c.rho_bits;
+    a.ctl = c.ctl;
+    a.multi = mult ? 1 : 0;
+    auto fam = [&](SorFam &f, const Geo &g, const double *b, const uint8_t *flag, const BBox &box,
+                   const double *cE, const double *cW, const double *cD, const double *cN, const double *cS, int ui0,
+                   int ui1, int uj0, int uj1) {
+      f.g = g; f.b = b; f.flag = flag; f.box = box;
+      f.cE = cE; f.cW = cW; f.cD = cD; f.cN = cN; f.cS = cS;
+      f.ui0 = ui0; f.ui1 = ui1; f.uj0 = uj0; f.uj1 = uj1;
+      f.tiles_x = (g.ni + 127) / 128;
+      f.tiles_y = (g.nj + 15) / 16;
+    };
+    const Metric &m = c.m;
+    if (helm) {
+      fam(a.f[0], s.gu, s.ru, s.tu, s.bu, m.cEu, m.cWu, m.cDu, m.cNu, m.cSu, 1, c.nx, 0, c.ny);
+      fam(a.f[1], s.gv, s.rv, s.tv, s.bv, m.cEv, m.cWv, m.cDv, m.cNv, m.cSv, 0, c.nx, 1, c.ny);
+      a.nfam = 2;
+    } else {
+      BBox pb = s.bpb;
+      fam(a.f[0], s.gp, s.bp, s.pf, pb, m.cEp, m.cWp, m.cDp, m.cNp, m.cSp, 0, c.nx, 0, c.ny);
+      a.nfam = 1;
+    }
+    a.total_tiles = a.f[0].tiles_x * a.f[0].tiles_y + (a.nfam == 2 ? a.f[1].tiles_x * a.f[1].tiles_y : 0);
+    grids[r] = sor_grid(a);
+  }
+  int &hint = helm ? c.hint_uv : c.hint_p;
+  int batch = cfg.sor_batch > 0 ? cfg.sor_batch : std::max(4, std::min(hint, maxit));
+  int k = 1;
+  for (;;) {
+    const int kend = std::min(maxit, k + batch - 1);
+    for (int kk = k; kk <= kend; ++kk) {
+      const int in = (s0 + kk - 1) & 1, out = (s0 + kk) & 1;
+      if (mult) {
+        if (helm) {
+          HALO((*b = s.us[in], *g = &s.gu));
+          HALO((*b = s.vs[in], *g = &s.gv));
+        } else {
+          HALO((*b = s.phi[in], *g = &s.gp));
+        }
+      }
+      for (size_t r = 0; r < c.sl.size(); ++r) {
+        Slab &s = c.sl[r];
+        SorArgs &a = args[r];
+        a.k = kk;
+        if (helm) {
+          a.f[0].xin = s.us[in]; a.f[0].xout = s.us[out];
+          a.f[1].xin = s.vs[in]; a.f[1].xout = s.vs[out];
+        } else {
+          a.f[0].xin = s.phi[in]; a.f[0].xout = s.phi[out];
+        }
+        launch_sor_iteration(a, c.stream, grids[r]);
+      }
+      if (mult) {
+        if (!c.loopback)
+          NK(ncclAllReduce(c.rho_bits + kk, c.rho_bits + kk, 1, ncclUint64, ncclMax, (ncclComm_t)c.nccl, c.stream));
+        launch_sor_check(c.ctl, c.rho_bits, kk, maxit, cfg.check_every, tol, c.stream);
+      }
+    }
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(&c.h_ctl[0], c.ctl, sizeof(SorCtl), cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    if (c.h_ctl[0].k_done >= 0) break;
+    k = kend + 1;
+    if (cfg.sor_batch <= 0) batch = std::min(2 * batch, 1024);
+  }
+  *k_out = c.h_ctl[0].k_done;
+  unsigned long long rb = c.h_ctl[0].rho_final;
+  std::memcpy(rho_out, &rb, sizeof(double));
+  *status = c.h_ctl[0].status;
+  if (iters_override <= 0) hint = *k_out;
+  return IBM_OK;
+}
+
+float ev_ms(Ctx &c, int a, int b) {
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, c.ev[a], c.ev[b]) != cudaSuccess) ms = 0.f;
+  return ms;
+}
+
+// ---------------------------------------------------------------- one step n -> n+1
+int step_once(Ctx &c, ibm_step_stats *st) {
+  const double dt = c.cfg.dt;
+  const double t1 = (double)(c.step + 1) * dt;  // R13: not accumulated
+  double disp = 0.0, vb = 0.0;
+  if (c.body.has) plunge(t1, c.body.hbar, c.body.k, &disp, &vb);
+  const double yb = c.body.y0 + disp;
+  int status = IBM_OK;
+  CK(cudaEventRecord(c.ev[0], c.stream));
+  // a1 classification at t^{n+1} (R15) + Poisson masks
+  if (c.body.has)
+    for (Slab &s : c.sl) {
+      launch_classify(c, s, yb);
+      launch_pflags(c, s);
+    }
+  // N1 halos of u^n, v^n, p^n, then a2/a3 predictor
+  if (multi(c)) {
+    HALO((*b = s.u, *g = &s.gu));
+    HALO((*b = s.v, *g = &s.gv));
+    HALO((*b = s.p, *g = &s.gp));
+  }
+  for (Slab &s : c.sl) launch_predictor(c, s, yb, vb);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(c.ev[1], c.stream));
+  // a4 velocity (Helmholtz) SOR, u and v jointly (R5)
+  int ku = 0, sst = 0;
+  double rho_uv = 0.0;
+  int r = sor_solve(c, true, 0, &ku, &rho_uv, &sst, 0);
+  if (r) return r;
+  if (st) { st->it_uv = ku; st->rho_uv = rho_uv; }
+  if (sst == 3) { c.err = "velocity SOR residual is NaN at step " + std::to_string(c.step + 1); return IBM_ERR_DIVERGED; }
+  if (sst == 1) status = IBM_WARN_NOCONV;
+  const int ures = ku & 1;
+  for (Slab &s : c.sl) launch_outlet_fill(c, s, s.us[ures]);
+  if (multi(c)) {
+    HALO((*b = s.us[ures], *g = &s.gu));
+    HALO((*b = s.vs[ures], *g = &s.gv));
+  }
+  CK(cudaEventRecord(c.ev[2], c.stream));
+  // a5 masks -> q, Poisson rhs; phi := 0 on inactive cells
+  for (Slab &s : c.sl) launch_prhs(c, s, s.us[ures], s.vs[ures], s.phi[c.phi_cur]);
+  CK(cudaEventRecord(c.ev[3], c.stream));
+  // a6 Poisson SOR, warm start
+  int kp = 0;
+  double rho_p = 0.0;
+  r = sor_solve(c, false, c.phi_cur, &kp, &rho_p, &sst, 0);
+  if (r) return r;
+  if (st) { st->it_p = kp; st->rho_p = rho_p; }
+  if (sst == 3) { c.err = "pressure SOR residual is NaN at step " + std::to_string(c.step + 1); return IBM_ERR_DIVERGED; }
+  if (sst == 1) status = IBM_WARN_NOCONV;
+  c.phi_cur = (c.phi_cur + kp) & 1;
+  if (multi(c)) HALO((*b = s.phi[c.phi_cur], *g = &s.gp));
+  CK(cudaEventRecord(c.ev[4], c.stream));
+  // a7 projection
+  CK(cudaMemsetAsync(c.nanflag, 0, sizeof(int), c.stream));
+  for (Slab &s : c.sl) launch_correct(c, s, s.us[ures], s.vs[ures], s.phi[c.phi_cur]);
+  CK(cudaEventRecord(c.ev[5], c.stream));
+  // history rotation
+  for (Slab &s : c.sl) {
+    std::swap(s.cu, s.cup);
+    std::swap(s.cv, s.cvp);
+  }
+  c.have_hist = 1;
+  // a8 forces
+  for (Slab &s : c.sl) launch_forces(c, s);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(c.ev[6], c.stream));
+  double sums[4];
+  r = force_sums(c, sums);
+  if (r) return r;
+  const double Fx = -sums[0] + (sums[1] - c.Mx) / dt;
+  const double Fy = -sums[2] + (sums[3] - c.My) / dt;
+  c.Mx = sums[1];
+  c.My = sums[3];
+  c.last_t = t1;
+  c.last_cd = 2.0 * Fx;
+  c.last_cl = 2.0 * Fy;
+  c.step += 1;
+  if (st) {
+    st->step = c.step;
+    st->t_bar = t1;
+    st->cd = c.last_cd;
+    st->cl = c.last_cl;
+    st->ms[0] = ev_ms(c, 0, 1);
+    st->ms[1] = ev_ms(c, 1, 2);
+    st->ms[2] = ev_ms(c, 2, 3);
+    st->ms[3] = ev_ms(c, 3, 4);
+    st->ms[4] = ev_ms(c, 4, 5);
+    st->ms[5] = ev_ms(c, 5, 6);
+  }
+  if (*c.h_nan) {
+    c.err = "non-finite field after correction at step " + std::to_string(c.step);
+    return IBM_ERR_DIVERGED;
+  }
+  return status;
+}
+
+const char *kNoCtx = "ctx is NULL";
+
+}  // namespace
+
+// ================================================================ C ABI
+extern "C" {
+
+int ibm_workspace_size(const ibm_config *cfg, size_t *bytes) {
+  std::string why;
+  int st = check_config(cfg, why);
+  if (st) return st;
+  if (!bytes) return IBM_ERR_ARG;
+  Ctx c;
+  c.cfg = *cfg;
+  c.loopback = cfg->loopback;
+  if (cfg->loopback)
+    for (int r = 0; r < cfg->nranks; ++r) c.sl.push_back(make_slab(*cfg, r));
+  else
+    c.sl.push_back(make_slab(*cfg, cfg->rank));
+  *bytes = carve(c, nullptr);
+  return IBM_OK;
+}
+
+int ibm_nccl_unique_id(unsigned char out[128]) {
+  if (!out) return IBM_ERR_ARG;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return IBM_ERR_NCCL;
+  std::memcpy(out, id.internal, 128);
+  return IBM_OK;
+}
+
+int ibm_init(const ibm_config *cfg, void *d_workspace, size_t bytes, void *cuda_stream, ibm_ctx **out) {
+  if (!out) return IBM_ERR_ARG;
+  *out = nullptr;
+  std::string why;
+  int st = check_config(cfg, why);
+  if (st) {
+    fprintf(stderr, "ibm_init: %s\n", why.c_str());
+    return st;
+  }
+  ibm_ctx *cp = new (std::nothrow) ibm_ctx();
+  if (!cp) return IBM_ERR_ARG;
+  Ctx &c = *cp;
+  c.cfg = *cfg;
+  c.cfg.xn = c.cfg.yn = nullptr;
+  c.cfg.nccl_id = nullptr;
+  if (c.cfg.check_every < 1) c.cfg.check_every = 1;
+  c.nx = cfg->nx;
+  c.ny = cfg->ny;
+  c.nranks = cfg->nranks;
+  c.device = cfg->device;
+  c.loopback = cfg->loopback;
+  c.stream = (cudaStream_t)cuda_stream;
+  c.nccl = nullptr;
+  c.hint_uv = 16;
+  c.hint_p = 64;
+  if (c.loopback)
+    for (int r = 0; r < cfg->nranks; ++r) c.sl.push_back(make_slab(*cfg, r));
+  else
+    c.sl.push_back(make_slab(*cfg, cfg->rank));
+  auto fail = [&](int code) {
+    fprintf(stderr, "ibm_init: %s\n", c.err.c_str());
+    delete cp;
+    return code;
+  };
+  if (cudaSetDevice(c.device) != cudaSuccess) { c.err = "cudaSetDevice failed"; return fail(IBM_ERR_CUDA); }
+  const size_t need = carve(c, nullptr);
+  if (!d_workspace || bytes < need || ((uintptr_t)d_workspace & 255)) {
+    c.err = "workspace NULL, misaligned or too small (need " + std::to_string(need) + " B)";
+    return fail(IBM_ERR_ARG);
+  }
+  carve(c, (char *)d_workspace);
+  if (cudaHostAlloc((void **)&c.h_ctl, 2 * sizeof(SorCtl), cudaHostAllocDefault) != cudaSuccess ||
+      cudaHostAlloc((void **)&c.h_red, 4 * sizeof(double) * c.sl.size(), cudaHostAllocDefault) != cudaSuccess ||
+      cudaHostAlloc((void **)&c.h_nan, sizeof(int), cudaHostAllocDefault) != cudaSuccess) {
+    c.err = "cudaHostAlloc failed";
+    return fail(IBM_ERR_CUDA);
+  }
+  for (auto &e : c.ev)
+    if (cudaEventCreate(&e) != cudaSuccess) { c.err = "cudaEventCreate failed"; return fail(IBM_ERR_CUDA); }
+  HostMetric h = host_metric(*cfg);
+  c.h_xn = nullptr;
+  c.h_yn = nullptr;
+  auto up = [&](double *d, const std::vector<double> &v) {
+    return cudaMemcpyAsync(d, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice, c.stream);
+  };
+  cudaError_t e = cudaMemsetAsync(d_workspace, 0, need, c.stream);
+  const Metric &m = c.m;
+  const std::pair<double *, const std::vector<double> *> ups[] = {
+      {m.xn, &h.xn}, {m.yn, &h.yn}, {m.dx, &h.dx}, {m.dy, &h.dy}, {m.xc, &h.xc}, {m.yc, &h.yc},
+      {m.hxc, &h.hxc}, {m.hyc, &h.hyc}, {m.cEu, &h.cEu}, {m.cWu, &h.cWu}, {m.cDu, &h.cDu},
+      {m.cNu, &h.cNu}, {m.cSu, &h.cSu}, {m.cEv, &h.cEv}, {m.cWv, &h.cWv}, {m.cDv, &h.cDv},
+      {m.cNv, &h.cNv}, {m.cSv, &h.cSv}, {m.cEp, &h.cEp}, {m.cWp, &h.cWp}, {m.cDp, &h.cDp},
+      {m.cNp, &h.cNp}, {m.cSp, &h.cSp}};
+  for (auto &pr : ups)
+    if (e == cudaSuccess) e = up(pr.first, *pr.second);
+  if (e == cudaSuccess)
+    for (Slab &s : c.sl) launch_fill(s.u, s.gu, 1.0, c.stream);  // impulsive start (R11)
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c.stream);
+  if (e != cudaSuccess) {
+    c.err = std::string("init upload: ") + cudaGetErrorString(e);
+    return fail(IBM_ERR_CUDA);
+  }
+  if (c.nranks > 1 && !c.loopback) {
+    ncclUniqueId id;
+    std::memcpy(id.internal, cfg->nccl_id, 128);
+    ncclComm_t comm;
+    ncclResult_t nr = ncclCommInitRank(&comm, c.nranks, id, cfg->rank);
+    if (nr != ncclSuccess) {
+      c.err = std::string("ncclCommInitRank: ") + ncclGetErrorString(nr);
+      return fail(IBM_ERR_NCCL);
+    }
+    c.nccl = comm;
+  }
+  c.body = Body{0, 0, 0, 0, 0, 0, 0};
+  c.phi_cur = 0;
+  c.step = 0;
+  c.have_hist = 0;
+  c.Mx = c.My = 0.0;
+  c.last_t = c.last_cd = c.last_cl = 0.0;
+  // host copies of the family coordinates for the body boxes
+  c.h_xn = new double[c.nx + 1];
+  c.h_yn = new double[c.ny + 1];
+  std::memcpy(c.h_xn, cfg->xn, sizeof(double) * (c.nx + 1));
+  std::memcpy(c.h_yn, cfg->yn, sizeof(double) * (c.ny + 1));
+  *out = cp;
+  return IBM_OK;
+}
+
+static int set_body_impl(ibm_ctx *ctx, const Body &B) {
+  Ctx &c = *ctx;
+  CK(cudaSetDevice(c.device));
+  const int nx = c.nx, ny = c.ny;
+  const double *xn = c.h_xn, *yn = c.h_yn;
+  // zero tags, flags and forcing fields of the previous body
+  for (Slab &s : c.sl) {
+    CK(cudaMemsetAsync(s.tu, 0, s.gu.elems(), c.stream));
+    CK(cudaMemsetAsync(s.tv, 0, s.gv.elems(), c.stream));
+    CK(cudaMemsetAsync(s.tp, 0, s.gp.elems(), c.stream));
+    CK(cudaMemsetAsync(s.pf, 0, s.gp.elems(), c.stream));
+    CK(cudaMemsetAsync(s.fu, 0, s.gu.elems() * sizeof(double), c.stream));
+    CK(cudaMemsetAsync(s.fv, 0, s.gv.elems() * sizeof(double), c.stream));
+    s.bu = s.bv = s.bpb = BBox{0, 0, 0, 0};
+  }
+  c.body = B;
+  if (B.has) {
+    std::vector<double> vxn(xn, xn + nx + 1), vyn(yn, yn + ny + 1), vxc(nx), vyc(ny);
+    for (int i = 0; i < nx; ++i) vxc[i] = 0.5 * (xn[i] + xn[i + 1]);
+    for (int j = 0; j < ny; ++j) vyc[j] = 0.5 * (yn[j] + yn[j + 1]);
+    const double xlo = B.x0 - B.a, xhi = B.x0 + B.a;
+    const double ylo = B.y0 - B.hbar - B.b, yhi = B.y0 + B.hbar + B.b;
+    for (Slab &s : c.sl) {
+      s.bu = box_for(vxn, vyc, xlo, xhi, ylo, yhi, s.gu, 3);
+      s.bv = box_for(vxc, vyn, xlo, xhi, ylo, yhi, s.gv, 3);
+      s.bpb = box_for(vxc, vyc, xlo, xhi, ylo, yhi, s.gp, 3);
+    }
+  }
+  return refresh_time(c);
+}
+
+int ibm_set_body(ibm_ctx *ctx, double a, double b, double x0, double y0, double h_bar, double k) {
+  if (!ctx) return IBM_ERR_ARG;
+  Ctx &c = *ctx;
+  if (!(a > 0) || !(b > 0) || !(k > 0) || !(h_bar >= 0)) {
+    c.err = "body: a, b, k must be > 0 and h_bar >= 0";
+    return IBM_ERR_CONFIG;
+  }
+  const double *xn = c.h_xn, *yn = c.h_yn;
+  if (!(x0 - a > xn[3] && x0 + a < xn[c.nx - 3] && y0 - h_bar - b > yn[3] && y0 + h_bar + b < yn[c.ny - 3])) {
+    c.err = "body envelope must lie inside the domain by >= 3 cells";
+    return IBM_ERR_CONFIG;
+  }
+  return set_body_impl(ctx, Body{1, a, b, x0, y0, h_bar, k});
+}
+
+int ibm_clear_body(ibm_ctx *ctx) {
+  if (!ctx) return IBM_ERR_ARG;
+  return set_body_impl(ctx, Body{0, 0, 0, 0, 0, 0, 0});
+}
+
+// per-field device pointer / family geometry / element size
+static bool field_of(Slab &s, int bit, int phi_cur, void **ptr, const Geo **g, size_t *esz) {
+  *esz = sizeof(double);
+  switch (bit) {
+    case 0: *ptr = s.u; *g = &s.gu; return true;
+    case 1: *ptr = s.v; *g = &s.gv; return true;
+    case 2: *ptr = s.p; *g = &s.gp; return true;
+    case 3: *ptr = s.phi[phi_cur]; *g = &s.gp; return true;
+    case 4: *ptr = s.fu; *g = &s.gu; return true;
+    case 5: *ptr = s.fv; *g = &s.gv; return true;
+    case 6: *ptr = s.q; *g = &s.gp; return true;
+    case 7: *ptr = s.tu; *g = &s.gu; *esz = 1; return true;
+    case 8: *ptr = s.tv; *g = &s.gv; *esz = 1; return true;
+    case 9: *ptr = s.tp; *g = &s.gp; *esz = 1; return true;
+    case 10: *ptr = s.cup; *g = &s.gu; return true;
+    case 11: *ptr = s.cvp; *g = &s.gv; return true;
+  }
+  return false;
+}
+
+static int copy_fields(Ctx &c, unsigned mask, void *const *dst, const void *const *src, int where, bool get) {
+  const int base_row = c.loopback ? 0 : c.sl[0].pj0;
+  for (int bit = 0; bit < IBM_NFIELDS; ++bit) {
+    if (!(mask & (1u << bit))) continue;
+    void *user = get ? dst[bit] : const_cast<void *>(src[bit]);
+    if (!user) { c.err = "NULL buffer for field bit " + std::to_string(bit); return IBM_ERR_ARG; }
+    for (Slab &s : c.sl) {
+      void *dptr;
+      const Geo *g;
+      size_t esz;
+      field_of(s, bit, c.phi_cur, &dptr, &g, &esz);
+      char *dev = (char *)dptr + (size_t)g->off(0, 0) * esz;
+      char *hst = (char *)user + (size_t)(g->gj0 - base_row) * g->ni * esz;
+      const size_t wb = (size_t)g->ni * esz, pb = (size_t)g->pitch * esz;
+      cudaMemcpyKind kind = where == IBM_HOST ? (get ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice)
+                                              : cudaMemcpyDeviceToDevice;
+      if (get)
+        CK(cudaMemcpy2DAsync(hst, wb, dev, pb, wb, g->nj, kind, c.stream));
+      else
+        CK(cudaMemcpy2DAsync(dev, pb, hst, wb, wb, g->nj, kind, c.stream));
+    }
+  }
+  CK(cudaStreamSynchronize(c.stream));
+  return IBM_OK;
+}
+
+int ibm_set_fields(ibm_ctx *ctx, unsigned mask, const void *const *src, int where) {
+  if (!ctx) return IBM_ERR_ARG;
+  Ctx &c = *ctx;
+  const unsigned ok = IBM_U | IBM_V | IBM_P | IBM_PHI | IBM_CU_PREV | IBM_CV_PREV;
+  if (!src || (mask & ~ok)) { c.err = "set_fields: bad mask or NULL src"; return IBM_ERR_ARG; }
+  CK(cudaSetDevice(c.device));
+  return copy_fields(c, mask, nullptr, src, where, false);
+}
+
+int ibm_set_step(ibm_ctx *ctx, int step, int have_history) {
+  if (!ctx) return IBM_ERR_ARG;
+  Ctx &c = *ctx;
+  if (step < 0) { c.err = "step < 0"; return IBM_ERR_ARG; }
+  CK(cudaSetDevice(c.device));
+  c.step = step;
+  c.have_hist = have_history ? 1 : 0;
+  return refresh_time(c);
+}
+
+int ibm_step(ibm_ctx *ctx, int nsteps, ibm_step_stats *stats) {
+  if (!ctx) return IBM_ERR_STATE;
+  Ctx &c = *ctx;
+  if (nsteps < 0) return IBM_ERR_ARG;
+  CK(cudaSetDevice(c.device));
+  int worst = IBM_OK;
+  for (int n = 0; n < nsteps; ++n) {
+    ibm_step_stats local;
+    std::memset(&local, 0, sizeof(local));
+    int st = step_once(c, &local);
+    local.status = st;
+    if (stats) stats[n] = local;
+    if (st == IBM_ERR_DIVERGED || st > IBM_ERR_DIVERGED) return st;
+    if (st > worst) worst = st;
+  }
+  return worst;
+}
+
+int ibm_get_fields(ibm_ctx *ctx, unsigned mask, void *const *dst, int where, int *j0, int *j1) {
+  if (!ctx) return IBM_ERR_ARG;
+  Ctx &c = *ctx;
+  if (!dst || (mask >> IBM_NFIELDS)) { c.err = "get_fields: bad mask or NULL dst"; return IBM_ERR_ARG; }
+  CK(cudaSetDevice(c.device));
+  if (j0) *j0 = c.loopback ? 0 : c.sl[0].pj0;
+  if (j1) *j1 = c.loopback ? c.ny : c.sl[0].pj1;
+  return copy_fields(c, mask, dst, nullptr, where, true);
+}
+
+int ibm_forces(ibm_ctx *ctx, double out[3]) {
+  if (!ctx || !out) return IBM_ERR_ARG;
+  out[0] = ctx->last_t;
+  out[1] = ctx->last_cd;
+  out[2] = ctx->last_cl;
+  return IBM_OK;
+}
+
+int ibm_poisson_iterate(ibm_ctx *ctx, int iters, double *rho_out) {
+  if (!ctx) return IBM_ERR_STATE;
+  Ctx &c = *ctx;
+  if (iters < 1 || (size_t)iters + 2 > rho_len(c.cfg)) { c.err = "iters outside [1, max(maxit)]"; return IBM_ERR_ARG; }
+  CK(cudaSetDevice(c.device));
+  int k = 0, sst = 0;
+  double rho = 0.0;
+  int r = sor_solve(c, false, c.phi_cur, &k, &rho, &sst, iters);
+  if (r) return r;
+  c.phi_cur = (c.phi_cur + k) & 1;
+  if (rho_out) *rho_out = rho;
+  return sst == 3 ? IBM_ERR_DIVERGED : IBM_OK;
+}
+
+const char *ibm_last_error(const ibm_ctx *ctx) {
+  if (!ctx) return kNoCtx;
+  return ctx->err.c_str();
+}
+
+int ibm_destroy(ibm_ctx *ctx) {
+  if (!ctx) return IBM_ERR_ARG;
+  Ctx &c = *ctx;
+  cudaSetDevice(c.device);
+  cudaStreamSynchronize(c.stream);
+  if (c.nccl) ncclCommDestroy((ncclComm_t)c.nccl);
+  for (auto &e : c.ev) cudaEventDestroy(e);
+  cudaFreeHost(c.h_ctl);
+  cudaFreeHost(c.h_red);
+  cudaFreeHost(c.h_nan);
+  delete[] c.h_xn;
+  delete[] c.h_yn;
+  delete ctx;
+  return IBM_OK;
+}
+
+}  // extern "C"

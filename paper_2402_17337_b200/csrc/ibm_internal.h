@@ -1,0 +1,136 @@
+// Internal declarations of the B200 library (not part of the C ABI).
+// Layout of every staggered family in HBM: row-major, x fastest,
+// row pitch a multiple of 32 doubles (256 B), 2 ghost rows below and above the
+// slab's owned rows (the halo of the fused red-black pass); out-of-range
+// columns are never stored -- kernels treat them as 0 with coefficient 0,
+// exactly like the oracle's out-of-range reads.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/ibm.h"
+
+namespace ibm {
+
+constexpr int kGhost = 2;  // ghost rows per side
+enum Tag : uint8_t { FLUID = 0, SOLID = 1, FORCING = 2 };
+// Poisson cell flags; 0 = active cell with all four faces open (the default
+// outside the body envelope box).  Closed bits are only set on interior faces.
+enum PFlag : uint8_t { PF_INACTIVE = 1, PF_E = 2, PF_W = 4, PF_N = 8, PF_S = 16 };
+
+struct Geo {
+  int ni;      // columns of the family (global == local)
+  int nj;      // owned rows of the slab
+  int gj0;     // global row index of local row 0
+  int NJ;      // global rows of the family
+  long pitch;  // elements per stored row
+  __host__ __device__ long off(int i, int jl) const { return (long)(jl + kGhost) * pitch + i; }
+  __host__ __device__ long elems() const { return (long)(nj + 2 * kGhost) * pitch; }
+};
+
+struct BBox {  // half-open node-index box: global columns, LOCAL rows
+  int i0, i1, j0, j1;
+  __host__ __device__ bool contains(int i, int jl) const { return i >= i0 && i < i1 && jl >= j0 && jl < j1; }
+  __host__ __device__ bool empty() const { return i0 >= i1 || j0 >= j1; }
+};
+
+// One family of one red-black SOR system (Poisson: phi; Helmholtz: u* or v*).
+struct SorFam {
+  const double *xin;
+  double *xout;
+  const double *b;
+  const uint8_t *flag;  // pflags (Poisson) or tags (Helmholtz)
+  Geo g;
+  BBox box;
+  const double *cE, *cW, *cD;  // per global column
+  const double *cN, *cS;       // per global row
+  int ui0, ui1, uj0, uj1;      // updatable global index ranges [ui0, ui1) x [uj0, uj1)
+  int tiles_x, tiles_y;
+};
+
+struct SorCtl {  // per-solve device control block
+  unsigned long long rho_final;  // bits of rho at k_done
+  int k_done;                    // -1 until converged / stopped
+  int status;                    // 0 converged, 1 maxit, 3 NaN
+  unsigned ticket;               // last-block counter
+  int pad;
+};
+
+struct SorArgs {
+  SorFam f[2];
+  int nfam;
+  int helmholtz;  // 0: Poisson coefficients from flags; 1: beta * metric coefficients
+  double beta, omega, omc, tol;
+  int k, maxit, check_every;
+  int total_tiles;
+  unsigned long long *rho_bits;  // [maxit + 2], zeroed per solve
+  SorCtl *ctl;
+  int multi;  // 1: several slabs / ranks -> decision in k_sor_check after the reduction
+};
+
+struct Metric {  // device pointers, global index space
+  double *xn, *yn, *dx, *dy, *xc, *yc, *hxc, *hyc;
+  double *cEu, *cWu, *cDu, *cNu, *cSu;
+  double *cEv, *cWv, *cDv, *cNv, *cSv;
+  double *cEp, *cWp, *cDp, *cNp, *cSp;
+};
+
+struct Body {
+  int has;
+  double a, b, x0, y0, hbar, k;
+};
+
+struct Slab {
+  int rank;          // global slab index
+  int pj0, pj1;      // owned global p rows
+  Geo gu, gv, gp;
+  double *u, *v, *p, *phi[2], *cu, *cv, *cup, *cvp, *us[2], *vs[2], *ru, *rv, *bp, *fu, *fv, *q;
+  uint8_t *tu, *tv, *tp, *pf;
+  BBox bu, bv, bpb;  // body envelope boxes (local rows incl. ghosts), empty without body
+  double *red;       // force partial sums [4]
+};
+
+struct Ctx {
+  ibm_config cfg;
+  int nx, ny, nranks, device;
+  int loopback;      // all slabs in this process (test mode: halos by device copies)
+  cudaStream_t stream;
+  Metric m;
+  std::vector<Slab> sl;
+  unsigned long long *rho_bits;
+  SorCtl *ctl;
+  int *nanflag;
+  double *h_xn, *h_yn;
+  SorCtl *h_ctl;   // pinned
+  double *h_red;   // pinned [4 * slabs]
+  int *h_nan;      // pinned
+  Body body;
+  int phi_cur;
+  int step, have_hist;
+  double Mx, My;
+  double last_t, last_cd, last_cl;
+  int hint_uv, hint_p;
+  cudaEvent_t ev[8];
+  void *nccl;      // ncclComm_t when nranks > 1 and !loopback
+  std::string err;
+};
+
+// kernel launchers (kernels.cu)
+void launch_classify(const Ctx &c, const Slab &s, double yb);
+void launch_pflags(const Ctx &c, const Slab &s);
+void launch_predictor(const Ctx &c, const Slab &s, double yb, double vb);
+int sor_grid(const SorArgs &a);
+void launch_sor_iteration(const SorArgs &a, cudaStream_t st, int grid);
+void launch_sor_check(SorCtl *ctl, const unsigned long long *rho_bits, int k, int maxit, int check_every,
+                      double tol, cudaStream_t st);
+void launch_outlet_fill(const Ctx &c, const Slab &s, double *us);
+void launch_prhs(const Ctx &c, const Slab &s, const double *us, const double *vs, double *phi_start);
+void launch_correct(const Ctx &c, const Slab &s, const double *us, const double *vs, const double *phi);
+void launch_forces(const Ctx &c, const Slab &s);
+void launch_fill(double *p, const Geo &g, double val, cudaStream_t st);
+
+}  // namespace ibm

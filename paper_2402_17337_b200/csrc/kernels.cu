@@ -1,0 +1,745 @@
+// sm_100a fp64 kernels of the IBM fractional-step hot path.
+//
+// Arithmetic contract (reading R13): compiled with --fmad=false;
+// every expression keeps the parenthesisation written in DESIGN.md §3 so the
+// results are bit-identical to the CPU oracle; IEEE division and sqrt; no
+// transcendental functions on the device (sin/cos are evaluated on the host).
+//
+// Citations: P:NN = PAPER.md line NN, S:NN = SPEC.md line NN.
+#include <cstdint>
+
+#include "ibm_internal.h"
+
+namespace ibm {
+
+__device__ __forceinline__ double ld(const double *__restrict__ p, const Geo &g, int i, int jl) {
+  if (i < 0 || i >= g.ni || jl < -kGhost || jl >= g.nj + kGhost) return 0.0;
+  return __ldg(p + g.off(i, jl));
+}
+
+__device__ __forceinline__ double2 ld2(const double *__restrict__ p, const Geo &g, int i, int jl) {
+  double2 r = make_double2(0.0, 0.0);
+  if (jl < -kGhost || jl >= g.nj + kGhost) return r;
+  const double *row = p + (long)(jl + kGhost) * g.pitch;
+  if (i >= 0 && i + 1 < g.ni) return __ldg(reinterpret_cast<const double2 *>(row + i));
+  if (i >= 0 && i < g.ni) r.x = __ldg(row + i);
+  if (i + 1 >= 0 && i + 1 < g.ni) r.y = __ldg(row + i + 1);
+  return r;
+}
+
+// ---------------------------------------------------------------- a1: classification
+// Solid = inside the ellipse (boundary inclusive); Forcing = Solid
+// with at least one in-range 4-neighbour outside.  Recomputed analytically for the
+// neighbours, so one pass; runs over the body envelope box only (R12, R15).
+__global__ void k_classify(uint8_t *__restrict__ tag, Geo g, BBox box, const double *__restrict__ xs,
+                           const double *__restrict__ ys, double a, double b, double xb, double yb) {
+  int i = box.i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  int jl = box.j0 + blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= box.i1 || jl >= box.j1) return;
+  int gj = g.gj0 + jl;
+  auto ins = [&](int ii, int jj) -> bool {
+    double dxn = (xs[ii] - xb) / a;
+    double dyn = (ys[jj] - yb) / b;
+    double s = dxn * dxn + dyn * dyn;
+    return s <= 1.0;
+  };
+  uint8_t t = FLUID;
+  if (ins(i, gj)) {
+    bool fl = false;
+    if (i + 1 < g.ni && !ins(i + 1, gj)) fl = true;
+    if (i - 1 >= 0 && !ins(i - 1, gj)) fl = true;
+    if (gj + 1 < g.NJ && !ins(i, gj + 1)) fl = true;
+    if (gj - 1 >= 0 && !ins(i, gj - 1)) fl = true;
+    t = fl ? FORCING : SOLID;
+  }
+  tag[g.off(i, jl)] = t;
+}
+
+// ---------------------------------------------------------------- a5 masks (R16-R18)
+__global__ void k_pflags(uint8_t *__restrict__ pf, const uint8_t *__restrict__ tp, const uint8_t *__restrict__ tu,
+                         const uint8_t *__restrict__ tv, Geo gp, Geo gu, Geo gv, BBox box, Metric m, int nx,
+                         int ny) {
+  int i = box.i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  int jl = box.j0 + blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= box.i1 || jl >= box.j1) return;
+  int gj = gp.gj0 + jl;
+  auto act0 = [&](int ii, int jj) -> bool { return tp[gp.off(ii, jj)] == FLUID; };
+  bool a0 = act0(i, jl);
+  bool oE = (i + 1 <= nx - 1) && tu[gu.off(i + 1, jl)] == FLUID && a0 && act0(i + 1, jl);
+  bool oW = (i >= 1) && tu[gu.off(i, jl)] == FLUID && act0(i - 1, jl) && a0;
+  bool oN = (gj + 1 <= ny - 1) && tv[gv.off(i, jl + 1)] == FLUID && a0 && act0(i, jl + 1);
+  bool oS = (gj >= 1) && tv[gv.off(i, jl)] == FLUID && act0(i, jl - 1) && a0;
+  uint8_t f = 0;
+  if (i + 1 <= nx - 1 && !oE) f |= PF_E;
+  if (i >= 1 && !oW) f |= PF_W;
+  if (gj + 1 <= ny - 1 && !oN) f |= PF_N;
+  if (gj >= 1 && !oS) f |= PF_S;
+  bool act = a0;
+  if (act) {  // R18: zero Poisson diagonal -> inactive
+    double aE = oE ? m.cEp[i] : 0.0;
+    double aW = oW ? m.cWp[i] : 0.0;
+    double aN = oN ? m.cNp[gj] : 0.0;
+    double aS = oS ? m.cSp[gj] : 0.0;
+    double aP = ((aE + aW) + (aN + aS)) + m.cDp[i];
+    if (aP == 0.0) act = false;
+  }
+  if (!act) f |= PF_INACTIVE;
+  pf[gp.off(i, jl)] = f;
+}
+
+// ---------------------------------------------------------------- a3: forcing targets
+struct BodyNow {
+  double a, b, xb, yb, vb;
+};
+
+// R14 / R14b: average over E, W, N, S fluid neighbours of the 1-D
+// linear extrapolation from the boundary intercept B through the neighbour N
+// (through N2 = N + (N - F) when dN < dF), using u^n.
+__device__ double forcing_target(const double *__restrict__ x, const uint8_t *__restrict__ tag, const Geo &g,
+                                 const BBox &box, int i, int jl, const double *__restrict__ xs,
+                                 const double *__restrict__ ys, const BodyNow &B, double uB) {
+  const int gj = g.gj0 + jl;
+  const double xF = xs[i], yF = ys[gj];
+  double sum = 0.0;
+  int cnt = 0;
+#pragma unroll 1
+  for (int d = 0; d < 4; ++d) {
+    const int di = (d == 0) ? 1 : (d == 1) ? -1 : 0;
+    const int dj = (d == 2) ? 1 : (d == 3) ? -1 : 0;
+    int in_ = i + di, jn = gj + dj;
+    if (in_ < 0 || jn < 0 || in_ >= g.ni || jn >= g.NJ) continue;
+    int jnl = jn - g.gj0;
+    uint8_t tn = box.contains(in_, jnl) ? tag[g.off(in_, jnl)] : (uint8_t)FLUID;
+    if (tn != FLUID) continue;
+    double xN = xs[in_], yN = ys[jn];
+    double dF, dN;
+    if (d < 2) {
+      double eta = (yF - B.yb) / B.b;
+      double w = B.a * sqrt(1.0 - eta * eta);
+      double xB = di > 0 ? B.xb + w : B.xb - w;
+      dF = fabs(xB - xF);
+      dN = fabs(xN - xB);
+    } else {
+      double zeta = (xF - B.xb) / B.a;
+      double w = B.b * sqrt(1.0 - zeta * zeta);
+      double yB = dj > 0 ? B.yb + w : B.yb - w;
+      dF = fabs(yB - yF);
+      dN = fabs(yN - yB);
+    }
+    double uN = x[g.off(in_, jnl)];
+    if (dN < dF) {
+      int i2 = in_ + di, j2 = jn + dj;
+      if (i2 >= 0 && j2 >= 0 && i2 < g.ni && j2 < g.NJ) {
+        int j2l = j2 - g.gj0;
+        uint8_t t2 = box.contains(i2, j2l) ? tag[g.off(i2, j2l)] : (uint8_t)FLUID;
+        if (t2 == FLUID) {
+          dN = (d < 2) ? dN + fabs(xs[i2] - xN) : dN + fabs(ys[j2] - yN);
+          uN = x[g.off(i2, j2l)];
+        }
+      }
+    }
+    sum = sum + (uB - (uN - uB) * (dF / dN));
+    cnt = cnt + 1;
+  }
+  return sum / (double)cnt;
+}
+
+// ---------------------------------------------------------------- a2/a3: predictor
+struct PredArgs {
+  const double *u, *v, *p, *cup, *cvp;
+  double *cu, *cv, *ru, *rv, *us, *vs, *fu, *fv;
+  const uint8_t *tu, *tv;
+  Geo gu, gv, gp;
+  BBox bu, bv;
+  Metric m;
+  BodyNow B;
+  int nx, ny, have_hist;
+  double dt, halfnu, nu;
+};
+
+// u family: convection, AB2 (R8), grad p^n, explicit half of CN
+// (S:245), Helmholtz rhs at Fluid nodes; targets and f at Forcing nodes (R19);
+// body velocity at Solid nodes.
+__global__ void k_pred_u(PredArgs A) {
+  const Geo &g = A.gu;
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int jl = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= g.ni || jl >= g.nj) return;
+  const long o = g.off(i, jl);
+  const int gj = g.gj0 + jl, nx = A.nx, ny = A.ny;
+  const double *dx = A.m.dx, *dy = A.m.dy, *hxc = A.m.hxc;
+  if (i == 0 || i == nx) {
+    A.us[o] = A.u[o];
+    A.cu[o] = 0.0;
+    A.ru[o] = 0.0;
+    return;
+  }
+  const bool inbox = A.bu.contains(i, jl);
+  const uint8_t t = inbox ? A.tu[o] : (uint8_t)FLUID;
+  if (t == SOLID) {
+    A.us[o] = 0.0;
+    A.cu[o] = 0.0;
+    A.ru[o] = 0.0;
+    A.fu[o] = 0.0;
+    return;
+  }
+  const Geo &gv = A.gv, &gp = A.gp;
+  const double *u = A.u, *v = A.v;
+  const double uC = ld(u, g, i, jl);
+  const double uE = ld(u, g, i + 1, jl), uW = ld(u, g, i - 1, jl);
+  const double uN = ld(u, g, i, jl + 1), uS = ld(u, g, i, jl - 1);
+  // convection
+  double ue = 0.5 * (uC + uE);
+  double uw = 0.5 * (uW + uC);
+  double tn, ts;
+  if (gj == ny - 1) {
+    tn = 0.0;
+  } else {
+    double un = (dy[gj + 1] * uC + dy[gj] * uN) / (dy[gj] + dy[gj + 1]);
+    double vn = (dx[i] * ld(v, gv, i - 1, jl + 1) + dx[i - 1] * ld(v, gv, i, jl + 1)) / (dx[i - 1] + dx[i]);
+    tn = un * vn;
+  }
+  if (gj == 0) {
+    ts = 0.0;
+  } else {
+    double us_ = (dy[gj] * uS + dy[gj - 1] * uC) / (dy[gj - 1] + dy[gj]);
+    double vs_ = (dx[i] * ld(v, gv, i - 1, jl) + dx[i - 1] * ld(v, gv, i, jl)) / (dx[i - 1] + dx[i]);
+    ts = us_ * vs_;
+  }
+  const double C = (ue * ue - uw * uw) / hxc[i] + (tn - ts) / dy[gj];
+  const double Cp = A.have_hist ? A.cup[o] : C;
+  const double G = (ld(A.p, gp, i, jl) - ld(A.p, gp, i - 1, jl)) / hxc[i];
+  const double cE = A.m.cEu[i], cW = A.m.cWu[i], cD = A.m.cDu[i], cN = A.m.cNu[gj], cS = A.m.cSu[gj];
+  const double L = ((cE * (uE - uC) + cW * (uW - uC)) + (cN * (uN - uC) + cS * (uS - uC))) - cD * uC;
+  A.cu[o] = C;
+  if (t == FLUID) {
+    A.ru[o] = uC + A.dt * ((-(1.5 * C - 0.5 * Cp) - G) + A.halfnu * L);
+    A.us[o] = uC;
+    if (inbox) A.fu[o] = 0.0;
+  } else {  // FORCING
+    double tgt = forcing_target(u, A.tu, g, A.bu, i, jl, A.m.xn, A.m.yc, A.B, 0.0);
+    double uhat = uC + A.dt * ((-(1.5 * C - 0.5 * Cp) - G) + A.nu * L);
+    A.us[o] = tgt;
+    A.fu[o] = (tgt - uhat) / A.dt;
+    A.ru[o] = 0.0;
+  }
+}
+
+__global__ void k_pred_v(PredArgs A) {
+  const Geo &g = A.gv;
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int jl = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= g.ni || jl >= g.nj) return;
+  const long o = g.off(i, jl);
+  const int gj = g.gj0 + jl, nx = A.nx, ny = A.ny;
+  const double *dx = A.m.dx, *dy = A.m.dy, *hyc = A.m.hyc;
+  if (gj == 0 || gj == ny) {
+    A.vs[o] = A.v[o];
+    A.cv[o] = 0.0;
+    A.rv[o] = 0.0;
+    return;
+  }
+  const bool inbox = A.bv.contains(i, jl);
+  const uint8_t t = inbox ? A.tv[o] : (uint8_t)FLUID;
+  if (t == SOLID) {
+    A.vs[o] = A.B.vb;
+    A.cv[o] = 0.0;
+    A.rv[o] = 0.0;
+    A.fv[o] = 0.0;
+    return;
+  }
+  const Geo &gu = A.gu, &gp = A.gp;
+  const double *u = A.u, *v = A.v;
+  const double vC = ld(v, g, i, jl);
+  const double vE = ld(v, g, i + 1, jl), vW = ld(v, g, i - 1, jl);
+  const double vN = ld(v, g, i, jl + 1), vS = ld(v, g, i, jl - 1);
+  double vn = 0.5 * (vC + vN);
+  double vs_ = 0.5 * (vS + vC);
+  double ue = (dy[gj] * ld(u, gu, i + 1, jl - 1) + dy[gj - 1] * ld(u, gu, i + 1, jl)) / (dy[gj - 1] + dy[gj]);
+  double ve = (i == nx - 1) ? vC : (dx[i + 1] * vC + dx[i] * vE) / (dx[i] + dx[i + 1]);
+  double te = ue * ve, tw;
+  if (i == 0) {
+    tw = 0.0;  // inlet corner: u = 1, v = 0
+  } else {
+    double uw = (dy[gj] * ld(u, gu, i, jl - 1) + dy[gj - 1] * ld(u, gu, i, jl)) / (dy[gj - 1] + dy[gj]);
+    double vw = (dx[i] * vW + dx[i - 1] * vC) / (dx[i - 1] + dx[i]);
+    tw = uw * vw;
+  }
+  const double C = (te - tw) / dx[i] + (vn * vn - vs_ * vs_) / hyc[gj];
+  const double Cp = A.have_hist ? A.cvp[o] : C;
+  const double G = (ld(A.p, gp, i, jl) - ld(A.p, gp, i, jl - 1)) / hyc[gj];
+  const double cE = A.m.cEv[i], cW = A.m.cWv[i], cD = A.m.cDv[i], cN = A.m.cNv[gj], cS = A.m.cSv[gj];
+  const double L = ((cE * (vE - vC) + cW * (vW - vC)) + (cN * (vN - vC) + cS * (vS - vC))) - cD * vC;
+  A.cv[o] = C;
+  if (t == FLUID) {
+    A.rv[o] = vC + A.dt * ((-(1.5 * C - 0.5 * Cp) - G) + A.halfnu * L);
+    A.vs[o] = vC;
+    if (inbox) A.fv[o] = 0.0;
+  } else {
+    double tgt = forcing_target(v, A.tv, g, A.bv, i, jl, A.m.xc, A.m.yn, A.B, A.B.vb);
+    double vhat = vC + A.dt * ((-(1.5 * C - 0.5 * Cp) - G) + A.nu * L);
+    A.vs[o] = tgt;
+    A.fv[o] = (tgt - vhat) / A.dt;
+    A.rv[o] = 0.0;
+  }
+}
+
+// ---------------------------------------------------------------- a4/a6: red-black SOR
+// One launch = one full red-black iteration (R1-R3), fused in one HBM
+// pass: each CTA tile (TX x TY owned nodes) stages x and b with a 2-node halo in
+// shared memory, updates red on the tile plus a 1-node ring (recomputed
+// redundantly, bit-identical to the neighbour's own update), then black on the
+// tile, and writes the whole tile to the other ping-pong buffer.  The scaled
+// residual |gs - x_old| is max-reduced on its uint64 bit pattern (exact,
+// NaN-propagating) warp -> block -> atomicMax; the last CTA takes the
+// convergence decision for iteration k on the device (no host round-trip).
+constexpr int TX = 128, TY = 16, SW = TX + 4, SH = TY + 4, NT = 256;
+
+struct SorSmem {
+  double x[SH][SW];
+  double b[SH][SW];
+  double cE[SW], cW[SW], cD[SW], cN[SH], cS[SH];
+  uint8_t f[SH][SW];
+};
+
+__device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) {
+  return a > b ? a : b;
+}
+
+template <int HELM>
+__device__ __forceinline__ void sor_tile(const SorFam &F, SorSmem &S, int tt, const SorArgs &A,
+                                         unsigned long long &tmax) {
+  const int tx = tt % F.tiles_x, ty = tt / F.tiles_x;
+  const int i0 = tx * TX, j0 = ty * TY;
+  const Geo g = F.g;
+  const bool hasf = !F.box.empty() && (i0 - 2 < F.box.i1) && (i0 + TX + 2 > F.box.i0) && (j0 - 1 < F.box.j1) &&
+                    (j0 + TY + 1 > F.box.j0);
+  __syncthreads();  // previous tile done with smem
+  for (int idx = threadIdx.x; idx < SH * (SW / 2); idx += NT) {
+    const int r = idx / (SW / 2), cp = idx - r * (SW / 2);
+    const int jl = j0 - 2 + r, i = i0 - 2 + 2 * cp;
+    const double2 xv = ld2(F.xin, g, i, jl);
+    S.x[r][2 * cp] = xv.x;
+    S.x[r][2 * cp + 1] = xv.y;
+    if (r >= 1 && r <= SH - 2) {
+      const double2 bv = ld2(F.b, g, i, jl);
+      S.b[r][2 * cp] = bv.x;
+      S.b[r][2 * cp + 1] = bv.y;
+    }
+  }
+  for (int c = threadIdx.x; c < SW; c += NT) {
+    const int gi = i0 - 2 + c;
+    const bool ok = gi >= 0 && gi < g.ni;
+    S.cE[c] = ok ? F.cE[gi] : 0.0;
+    S.cW[c] = ok ? F.cW[gi] : 0.0;
+    S.cD[c] = ok ? F.cD[gi] : 0.0;
+  }
+  for (int r = threadIdx.x; r < SH; r += NT) {
+    const int gj = g.gj0 + j0 - 2 + r;
+    const bool ok = gj >= 0 && gj < g.NJ;
+    S.cN[r] = ok ? F.cN[gj] : 0.0;
+    S.cS[r] = ok ? F.cS[gj] : 0.0;
+  }
+  if (hasf) {
+    for (int idx = threadIdx.x; idx < (SH - 2) * SW; idx += NT) {
+      const int r = 1 + idx / SW, c = idx - (r - 1) * SW;
+      const int jl = j0 - 2 + r, i = i0 - 2 + c;
+      uint8_t fv = 0;
+      if (i >= 0 && i < g.ni && jl >= -kGhost && jl < g.nj + kGhost) fv = F.flag[g.off(i, jl)];
+      S.f[r][c] = fv;
+    }
+  }
+  __syncthreads();
+  const double omega = A.omega, omc = A.omc, beta = A.beta;
+  // red sweep on the tile and its 1-node ring (rows j0-1 .. j0+TY)
+  for (int idx = threadIdx.x; idx < (SH - 2) * (SW / 2); idx += NT) {
+    const int r = 1 + idx / (SW / 2), cp = idx - (r - 1) * (SW / 2);
+    const int jl = j0 - 2 + r, gj = g.gj0 + jl;
+    const int c = 2 * cp + (gj & 1);
+    if (c < 1 || c > SW - 2 || jl < -1 || jl > g.nj) continue;
+    const int gi = i0 - 2 + c;
+    if (gi < F.ui0 || gi >= F.ui1 || gj < F.uj0 || gj >= F.uj1) continue;
+    const uint8_t fl = hasf ? S.f[r][c] : (uint8_t)0;
+    double aE, aW, aN, aS, aP;
+    if (HELM) {
+      if (fl != FLUID) continue;
+      const double cE = S.cE[c], cW = S.cW[c], cN = S.cN[r], cS = S.cS[r], cD = S.cD[c];
+      aE = beta * cE; aW = beta * cW; aN = beta * cN; aS = beta * cS;
+      aP = 1.0 + beta * (((cE + cW) + (cN + cS)) + cD);
+    } else {
+      if (fl & PF_INACTIVE) continue;
+      aE = (fl & PF_E) ? 0.0 : S.cE[c];
+      aW = (fl & PF_W) ? 0.0 : S.cW[c];
+      aN = (fl & PF_N) ? 0.0 : S.cN[r];
+      aS = (fl & PF_S) ? 0.0 : S.cS[r];
+      aP = ((aE + aW) + (aN + aS)) + S.cD[c];
+    }
+    const double xo = S.x[r][c];
+    const double s = (aE * S.x[r][c + 1] + aW * S.x[r][c - 1]) + (aN * S.x[r + 1][c] + aS * S.x[r - 1][c]);
+    const double gs = (S.b[r][c] + s) / aP;
+    S.x[r][c] = omc * xo + omega * gs;
+    if (r >= 2 && r <= SH - 3 && c >= 2 && c <= SW - 3 && jl < g.nj)
+      tmax = umax64(tmax, (unsigned long long)__double_as_longlong(fabs(gs - xo)));
+  }
+  __syncthreads();
+  // black sweep on the tile (rows j0 .. j0+TY-1)
+  for (int idx = threadIdx.x; idx < (SH - 4) * (SW / 2); idx += NT) {
+    const int r = 2 + idx / (SW / 2), cp = idx - (r - 2) * (SW / 2);
+    const int jl = j0 - 2 + r, gj = g.gj0 + jl;
+    const int c = 2 * cp + 1 - (gj & 1);
+    if (c < 2 || c > SW - 3 || jl >= g.nj) continue;
+    const int gi = i0 - 2 + c;
+    if (gi < F.ui0 || gi >= F.ui1 || gj < F.uj0 || gj >= F.uj1) continue;
+    const uint8_t fl = hasf ? S.f[r][c] : (uint8_t)0;
+    double aE, aW, aN, aS, aP;
+    if (HELM) {
+      if (fl != FLUID) continue;
+      const double cE = S.cE[c], cW = S.cW[c], cN = S.cN[r], cS = S.cS[r], cD = S.cD[c];
+      aE = beta * cE; aW = beta * cW; aN = beta * cN; aS = beta * cS;
+      aP = 1.0 + beta * (((cE + cW) + (cN + cS)) + cD);
+    } else {
+      if (fl & PF_INACTIVE) continue;
+      aE = (fl & PF_E) ? 0.0 : S.cE[c];
+      aW = (fl & PF_W) ? 0.0 : S.cW[c];
+      aN = (fl & PF_N) ? 0.0 : S.cN[r];
+      aS = (fl & PF_S) ? 0.0 : S.cS[r];
+      aP = ((aE + aW) + (aN + aS)) + S.cD[c];
+    }
+    const double xo = S.x[r][c];
+    const double s = (aE * S.x[r][c + 1] + aW * S.x[r][c - 1]) + (aN * S.x[r + 1][c] + aS * S.x[r - 1][c]);
+    const double gs = (S.b[r][c] + s) / aP;
+    S.x[r][c] = omc * xo + omega * gs;
+    tmax = umax64(tmax, (unsigned long long)__double_as_longlong(fabs(gs - xo)));
+  }
+  __syncthreads();
+  // store the owned tile (both colours, updated or not) to the output buffer
+  for (int idx = threadIdx.x; idx < TY * (TX / 2); idx += NT) {
+    const int rr = idx / (TX / 2), m = idx - rr * (TX / 2);
+    const int jl = j0 + rr, i = i0 + 2 * m;
+    if (jl >= g.nj || i >= g.ni) continue;
+    double *row = F.xout + (long)(jl + kGhost) * g.pitch;
+    const double a = S.x[rr + 2][2 * m + 2], b = S.x[rr + 2][2 * m + 3];
+    if (i + 1 < g.ni)
+      *reinterpret_cast<double2 *>(row + i) = make_double2(a, b);
+    else
+      row[i] = a;
+  }
+}
+
+__device__ __forceinline__ void sor_decide(SorCtl *ctl, unsigned long long rb, int k, int maxit, int ce, double tol) {
+  const double rho = __longlong_as_double((long long)rb);
+  const bool nan_ = isnan(rho);
+  const bool conv = (k % ce == 0) && rho <= tol;
+  if (nan_ || conv || k >= maxit) {
+    ctl->rho_final = rb;
+    ctl->status = nan_ ? 3 : (conv ? 0 : 1);
+    __threadfence();
+    ctl->k_done = k;
+  }
+}
+
+template <int HELM>
+__global__ void __launch_bounds__(NT) k_sor(const SorArgs A) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  SorSmem &S = *reinterpret_cast<SorSmem *>(smraw);
+  __shared__ unsigned long long wmax[NT / 32];
+  if (*(volatile int *)&A.ctl->k_done >= 0) return;  // converged at an earlier iteration
+  unsigned long long tmax = 0;
+  const int nt0 = A.f[0].tiles_x * A.f[0].tiles_y;
+  for (int t = blockIdx.x; t < A.total_tiles; t += gridDim.x) {
+    if (t < nt0)
+      sor_tile<HELM>(A.f[0], S, t, A, tmax);
+    else
+      sor_tile<HELM>(A.f[1], S, t - nt0, A, tmax);
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) tmax = umax64(tmax, __shfl_xor_sync(0xffffffffu, tmax, off));
+  if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = tmax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long mx = 0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) mx = umax64(mx, wmax[w]);
+    if (mx) atomicMax(&A.rho_bits[A.k], mx);
+    if (!A.multi) {
+      __threadfence();
+      const unsigned tk = atomicAdd(&A.ctl->ticket, 1u);
+      if (tk == gridDim.x - 1) {
+        const unsigned long long rb = atomicAdd(&A.rho_bits[A.k], 0ull);
+        A.ctl->ticket = 0;
+        sor_decide(A.ctl, rb, A.k, A.maxit, A.check_every, A.tol);
+      }
+    }
+  }
+}
+
+// multi-rank variant of the decision: runs after the rho all-reduce
+__global__ void k_sor_check(SorCtl *ctl, const unsigned long long *rho_bits, int k, int maxit, int ce, double tol) {
+  if (ctl->k_done >= 0) return;
+  sor_decide(ctl, rho_bits[k], k, maxit, ce, tol);
+}
+
+// ---------------------------------------------------------------- outlet fill (R10)
+__global__ void k_outlet_fill(double *__restrict__ us, Geo g, int nx) {
+  int jl = blockIdx.x * blockDim.x + threadIdx.x;
+  if (jl >= g.nj) return;
+  us[g.off(nx, jl)] = us[g.off(nx - 1, jl)];
+}
+
+// ---------------------------------------------------------------- a5: Poisson rhs and q
+// S:269-277, R16: rhs = D_open(u*)/dt with domain-boundary faces always
+// counted; q = closed-face flux / V; b = -rhs; phi := 0 on inactive cells (R17).
+__global__ void k_prhs(const double *__restrict__ us, const double *__restrict__ vs, double *__restrict__ bp,
+                       double *__restrict__ q, double *__restrict__ phi0, const uint8_t *__restrict__ pf, Geo gp,
+                       Geo gu, Geo gv, BBox box, Metric m, int nx, int ny, double dt) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int jl = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= gp.ni || jl >= gp.nj) return;
+  const long o = gp.off(i, jl);
+  const int gj = gp.gj0 + jl;
+  const uint8_t f = box.contains(i, jl) ? pf[o] : (uint8_t)0;
+  if (f & PF_INACTIVE) {
+    q[o] = 0.0;
+    bp[o] = 0.0;
+    phi0[o] = 0.0;
+    return;
+  }
+  const double uE = us[gu.off(i + 1, jl)], uW = us[gu.off(i, jl)];
+  const double vN = vs[gv.off(i, jl + 1)], vS = vs[gv.off(i, jl)];
+  const double mE = (i + 1 == nx) ? 1.0 : ((f & PF_E) ? 0.0 : 1.0);
+  const double mW = (i == 0) ? 1.0 : ((f & PF_W) ? 0.0 : 1.0);
+  const double mN = (gj + 1 == ny) ? 1.0 : ((f & PF_N) ? 0.0 : 1.0);
+  const double mS = (gj == 0) ? 1.0 : ((f & PF_S) ? 0.0 : 1.0);
+  const double dxi = m.dx[i], dyj = m.dy[gj];
+  const double rhs = (((mE * uE - mW * uW) / dxi) + ((mN * vN - mS * vS) / dyj)) / dt;
+  q[o] = (((1.0 - mE) * uE - (1.0 - mW) * uW) / dxi) + (((1.0 - mN) * vN - (1.0 - mS) * vS) / dyj);
+  bp[o] = -rhs;
+}
+
+// ---------------------------------------------------------------- a7: projection
+// S:296-304, R9, R16: open faces u = u* - dt (phi_E - phi_W)/h; the outlet face
+// uses phi = 0 at the face; closed faces keep u*; p += phi on active cells.
+// Non-finite results raise the NaN flag.
+__global__ void k_correct_u(double *__restrict__ u, const double *__restrict__ us, const double *__restrict__ phi,
+                            const uint8_t *__restrict__ pf, Geo gu, Geo gp, BBox pbox, Metric m, int nx, double dt,
+                            int *nanflag) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int jl = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= gu.ni || jl >= gu.nj) return;
+  const long o = gu.off(i, jl);
+  double val = us[o];
+  if (i >= 1 && i <= nx - 1) {
+    const uint8_t f = pbox.contains(i, jl) ? pf[gp.off(i, jl)] : (uint8_t)0;
+    if (!(f & PF_W)) val = us[o] - dt * ((phi[gp.off(i, jl)] - phi[gp.off(i - 1, jl)]) / m.hxc[i]);
+  } else if (i == nx) {
+    const uint8_t f = pbox.contains(nx - 1, jl) ? pf[gp.off(nx - 1, jl)] : (uint8_t)0;
+    if (!(f & PF_INACTIVE)) val = us[o] - dt * ((0.0 - phi[gp.off(nx - 1, jl)]) / (0.5 * m.dx[nx - 1]));
+  }
+  u[o] = val;
+  if (!isfinite(val)) atomicOr(nanflag, 1);
+}
+
+__global__ void k_correct_v(double *__restrict__ v, const double *__restrict__ vs, const double *__restrict__ phi,
+                            const uint8_t *__restrict__ pf, Geo gv, Geo gp, BBox pbox, Metric m, int ny, double dt,
+                            int *nanflag) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int jl = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= gv.ni || jl >= gv.nj) return;
+  const long o = gv.off(i, jl);
+  const int gj = gv.gj0 + jl;
+  double val = vs[o];
+  if (gj >= 1 && gj <= ny - 1) {
+    const uint8_t f = pbox.contains(i, jl) ? pf[gp.off(i, jl)] : (uint8_t)0;
+    if (!(f & PF_S)) val = vs[o] - dt * ((phi[gp.off(i, jl)] - phi[gp.off(i, jl - 1)]) / m.hyc[gj]);
+  }
+  v[o] = val;
+  if (!isfinite(val)) atomicOr(nanflag, 1);
+}
+
+__global__ void k_correct_p(double *__restrict__ p, const double *__restrict__ phi, const uint8_t *__restrict__ pf,
+                            Geo gp, BBox pbox, int *nanflag) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int jl = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= gp.ni || jl >= gp.nj) return;
+  const long o = gp.off(i, jl);
+  const uint8_t f = pbox.contains(i, jl) ? pf[o] : (uint8_t)0;
+  double val = p[o];
+  if (!(f & PF_INACTIVE)) val = p[o] + phi[o];
+  p[o] = val;
+  if (!isfinite(val)) atomicOr(nanflag, 1);
+}
+
+// ---------------------------------------------------------------- a8: forces (R20)
+// red[0] = sum_Forcing f_u dV, red[1] = sum_{Solid,Forcing} u dV, red[2], red[3] for v.
+// One CTA over the body boxes: fixed reduction order (deterministic).
+__global__ void __launch_bounds__(512) k_forces(const double *__restrict__ u, const double *__restrict__ v,
+                                                const double *__restrict__ fu, const double *__restrict__ fv,
+                                                const uint8_t *__restrict__ tu, const uint8_t *__restrict__ tv,
+                                                Geo gu, Geo gv, BBox bu, BBox bv, Metric m, int nx, int ny,
+                                                double *red) {
+  __shared__ double sh[4][512];
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  {
+    const int w = bu.i1 - bu.i0, n = w * (bu.j1 - bu.j0);
+    for (int idx = threadIdx.x; idx < n && w > 0; idx += blockDim.x) {
+      const int i = bu.i0 + idx % w, jl = bu.j0 + idx / w;
+      if (i < 1 || i > nx - 1 || jl < 0 || jl >= gu.nj) continue;
+      const long o = gu.off(i, jl);
+      const uint8_t t = tu[o];
+      if (t == FLUID) continue;
+      const double dV = m.hxc[i] * m.dy[gu.gj0 + jl];
+      s1 = s1 + u[o] * dV;
+      if (t == FORCING) s0 = s0 + fu[o] * dV;
+    }
+  }
+  {
+    const int w = bv.i1 - bv.i0, n = w * (bv.j1 - bv.j0);
+    for (int idx = threadIdx.x; idx < n && w > 0; idx += blockDim.x) {
+      const int i = bv.i0 + idx % w, jl = bv.j0 + idx / w;
+      const int gj = gv.gj0 + jl;
+      if (gj < 1 || gj > ny - 1 || jl < 0 || jl >= gv.nj) continue;
+      const long o = gv.off(i, jl);
+      const uint8_t t = tv[o];
+      if (t == FLUID) continue;
+      const double dV = m.dx[i] * m.hyc[gj];
+      s3 = s3 + v[o] * dV;
+      if (t == FORCING) s2 = s2 + fv[o] * dV;
+    }
+  }
+  sh[0][threadIdx.x] = s0;
+  sh[1][threadIdx.x] = s1;
+  sh[2][threadIdx.x] = s2;
+  sh[3][threadIdx.x] = s3;
+  __syncthreads();
+  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st)
+      for (int q = 0; q < 4; ++q) sh[q][threadIdx.x] = sh[q][threadIdx.x] + sh[q][threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x < 4) red[threadIdx.x] = sh[threadIdx.x][0];
+}
+
+// fill the owned rows of a family with a constant (initial condition)
+__global__ void k_fill(double *__restrict__ p, Geo g, double val) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int jl = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= g.ni || jl >= g.nj) return;
+  p[g.off(i, jl)] = val;
+}
+
+// ================================================================ launchers
+static dim3 grid2(int ni, int nj, dim3 b) { return dim3((ni + b.x - 1) / b.x, (nj + b.y - 1) / b.y); }
+
+void launch_classify(const Ctx &c, const Slab &s, double yb) {
+  const Body &B = c.body;
+  struct F {
+    uint8_t *t;
+    const Geo *g;
+    const BBox *b;
+    const double *xs, *ys;
+  } fams[3] = {{s.tu, &s.gu, &s.bu, c.m.xn, c.m.yc}, {s.tv, &s.gv, &s.bv, c.m.xc, c.m.yn},
+               {s.tp, &s.gp, &s.bpb, c.m.xc, c.m.yc}};
+  for (auto &f : fams) {
+    if (f.b->empty()) continue;
+    // classification also covers the ghost rows inside the box (analytic, no exchange)
+    const BBox box = *f.b;
+    dim3 blk(32, 8);
+    k_classify<<<grid2(box.i1 - box.i0, box.j1 - box.j0, blk), blk, 0, c.stream>>>(f.t, *f.g, box, f.xs, f.ys, B.a,
+                                                                                     B.b, B.x0, yb);
+  }
+}
+
+void launch_pflags(const Ctx &c, const Slab &s) {
+  if (s.bpb.empty()) return;
+  // flags are needed on the owned rows and one ghost row each side
+  BBox box = s.bpb;
+  box.j0 = box.j0 < -1 ? -1 : box.j0;
+  box.j1 = box.j1 > s.gp.nj + 1 ? s.gp.nj + 1 : box.j1;
+  if (box.empty()) return;
+  dim3 blk(32, 8);
+  k_pflags<<<grid2(box.i1 - box.i0, box.j1 - box.j0, blk), blk, 0, c.stream>>>(s.pf, s.tp, s.tu, s.tv, s.gp, s.gu,
+                                                                                s.gv, box, c.m, c.nx, c.ny);
+}
+
+void launch_predictor(const Ctx &c, const Slab &s, double yb, double vb) {
+  PredArgs A;
+  A.u = s.u; A.v = s.v; A.p = s.p; A.cup = s.cup; A.cvp = s.cvp;
+  A.cu = s.cu; A.cv = s.cv; A.ru = s.ru; A.rv = s.rv; A.us = s.us[0]; A.vs = s.vs[0]; A.fu = s.fu; A.fv = s.fv;
+  A.tu = s.tu; A.tv = s.tv;
+  A.gu = s.gu; A.gv = s.gv; A.gp = s.gp;
+  A.bu = s.bu; A.bv = s.bv;
+  A.m = c.m;
+  A.B.a = c.body.a; A.B.b = c.body.b; A.B.xb = c.body.x0; A.B.yb = yb; A.B.vb = vb;
+  A.nx = c.nx; A.ny = c.ny; A.have_hist = c.have_hist;
+  A.dt = c.cfg.dt;
+  A.halfnu = 0.5 / c.cfg.Re;
+  A.nu = 1.0 / c.cfg.Re;
+  dim3 blk(128, 2);
+  k_pred_u<<<grid2(s.gu.ni, s.gu.nj, blk), blk, 0, c.stream>>>(A);
+  k_pred_v<<<grid2(s.gv.ni, s.gv.nj, blk), blk, 0, c.stream>>>(A);
+}
+
+static int g_sor_blocks[2] = {0, 0};
+
+int sor_grid(const SorArgs &a) {
+  const int h = a.helmholtz ? 1 : 0;
+  if (!g_sor_blocks[h]) {
+    const size_t smem = sizeof(SorSmem);
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (h) {
+      cudaFuncSetAttribute(k_sor<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sor<1>, NT, smem);
+    } else {
+      cudaFuncSetAttribute(k_sor<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sor<0>, NT, smem);
+    }
+    g_sor_blocks[h] = (per > 0 ? per : 1) * (sms > 0 ? sms : 1);
+  }
+  return a.total_tiles < g_sor_blocks[h] ? a.total_tiles : g_sor_blocks[h];
+}
+
+void launch_sor_iteration(const SorArgs &a, cudaStream_t s, int grid) {
+  const size_t smem = sizeof(SorSmem);
+  if (a.helmholtz)
+    k_sor<1><<<grid, NT, smem, s>>>(a);
+  else
+    k_sor<0><<<grid, NT, smem, s>>>(a);
+}
+
+void launch_sor_check(SorCtl *ctl, const unsigned long long *rho_bits, int k, int maxit, int check_every,
+                      double tol, cudaStream_t s) {
+  k_sor_check<<<1, 1, 0, s>>>(ctl, rho_bits, k, maxit, check_every, tol);
+}
+
+void launch_outlet_fill(const Ctx &c, const Slab &s, double *us) {
+  k_outlet_fill<<<(s.gu.nj + 127) / 128, 128, 0, c.stream>>>(us, s.gu, c.nx);
+}
+
+void launch_prhs(const Ctx &c, const Slab &s, const double *us, const double *vs, double *phi_start) {
+  dim3 blk(128, 2);
+  k_prhs<<<grid2(s.gp.ni, s.gp.nj, blk), blk, 0, c.stream>>>(us, vs, s.bp, s.q, phi_start, s.pf, s.gp, s.gu, s.gv,
+                                                             s.bpb, c.m, c.nx, c.ny, c.cfg.dt);
+}
+
+void launch_correct(const Ctx &c, const Slab &s, const double *us, const double *vs, const double *phi) {
+  dim3 blk(128, 2);
+  k_correct_u<<<grid2(s.gu.ni, s.gu.nj, blk), blk, 0, c.stream>>>(s.u, us, phi, s.pf, s.gu, s.gp, s.bpb, c.m, c.nx,
+                                                                  c.cfg.dt, c.nanflag);
+  k_correct_v<<<grid2(s.gv.ni, s.gv.nj, blk), blk, 0, c.stream>>>(s.v, vs, phi, s.pf, s.gv, s.gp, s.bpb, c.m, c.ny,
+                                                                  c.cfg.dt, c.nanflag);
+  k_correct_p<<<grid2(s.gp.ni, s.gp.nj, blk), blk, 0, c.stream>>>(s.p, phi, s.pf, s.gp, s.bpb, c.nanflag);
+}
+
+void launch_fill(double *p, const Geo &g, double val, cudaStream_t st) {
+  dim3 blk(128, 2);
+  k_fill<<<grid2(g.ni, g.nj, blk), blk, 0, st>>>(p, g, val);
+}
+
+void launch_forces(const Ctx &c, const Slab &s) {
+  k_forces<<<1, 512, 0, c.stream>>>(s.u, s.v, s.fu, s.fv, s.tu, s.tv, s.gu, s.gv, s.bu, s.bv, c.m, c.nx, c.ny,
+                                     s.red);
+}
+
+}  // namespace ibm

@@ -1,0 +1,251 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle on the same
+seeded inputs.  Gate (BASELINE.json north_star): relative L2 <= 1e-9 on the
+fields after 10 steps and <= 1e-8 on the force coefficients; internal gate:
+identical SOR iteration counts every step and bit-identical fields (same
+arithmetic).  Forces are sums in a different order, so they
+are compared with the tolerance only (reading R24 for the denominator)."""
+import math
+
+import numpy as np
+import pytest
+
+import ibm_inputs as I
+
+pytestmark = pytest.mark.gpu
+
+FIELD_TOL = 1e-9
+FORCE_TOL = 1e-8
+
+
+@pytest.fixture(scope="module")
+def mods(oracle_mod):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2402_17337_b200 import build as B
+    B.build()
+    import paper_2402_17337_b200 as P
+    return oracle_mod, P
+
+
+def rel_l2(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def run_pair(mods, cfg, steps, u0=None, v0=None, p0=None, **gkw):
+    O, P = mods
+    if u0 is None:
+        u0, v0, p0 = I.initial_fields(cfg.nx, cfg.ny, cfg.perturb, cfg.seed)
+    o = O.Oracle(cfg.xn, cfg.yn, **cfg.solver_kwargs())
+    g = P.Solver(cfg.xn, cfg.yn, device=0, **cfg.solver_kwargs(), **gkw)
+    if cfg.body is not None:
+        o.set_body(*cfg.body_args())
+        g.set_body(*cfg.body_args())
+    else:
+        o.clear_body()
+        g.clear_body()
+    o.set_fields(u0, v0, p0)
+    g.set_fields(u0, v0, p0)
+    so, sto = o.step(steps)
+    sg, stg = g.step(steps)
+    return o, g, (so, sto), (sg, stg)
+
+
+def assert_parity(o, g, rs_o, rs_g, bitwise=True, names=("u", "v", "p", "phi", "fu", "fv", "q")):
+    so, sto = rs_o
+    sg, stg = rs_g
+    assert sg == so, (sg, so)
+    # identical SOR iteration counts every step (velocity and pressure)
+    assert np.array_equal(stg[:, 1:3], sto[:, 1:3]), np.c_[stg[:, 1:3], sto[:, 1:3]]
+    assert np.array_equal(stg[:, 0], sto[:, 0])
+    for name in names:
+        a, b = g.get(name), o.get(name)
+        assert a.shape == b.shape
+        r = rel_l2(a, b)
+        assert r <= FIELD_TOL, (name, r)
+        if bitwise:
+            assert np.array_equal(a, b), (name, np.abs(a - b).max())
+    for name in ("tu", "tv", "tp"):
+        assert np.array_equal(g.get(name), o.get(name)), name
+    # force coefficients: relative to the RMS of the oracle's history (R24)
+    for col in (5, 6):
+        ref = sto[:, col]
+        scale = max(math.sqrt(np.mean(ref ** 2)), 1e-30)
+        assert np.abs(stg[:, col] - ref).max() / scale <= FORCE_TOL, (col, stg[:, col], ref)
+    # SOR residuals are exact maxima of identical values
+    assert np.array_equal(stg[:, 3:5], sto[:, 3:5])
+
+
+def test_cfg1_foil_10_steps(mods):
+    """BJ configs[0]: plunging foil Re=500, 128x96, 10 steps, perturbed impulsive start."""
+    cfg = I.cfg1()
+    o, g, ro, rg = run_pair(mods, cfg, cfg.steps)
+    assert_parity(o, g, ro, rg)
+    g.close()
+
+
+def test_cfg1_unperturbed(mods):
+    cfg = I.cfg1(perturb=0.0, steps=6)
+    o, g, ro, rg = run_pair(mods, cfg, cfg.steps)
+    assert_parity(o, g, ro, rg)
+
+
+@pytest.mark.parametrize("nx,ny", [(130, 98), (257, 131), (64, 36)])
+def test_ragged_tiles(mods, nx, ny):
+    """Grids that leave ragged tiles in x and y (tile = 128 x 16 nodes)."""
+    cfg = I.cfg1(nx=nx, ny=ny, steps=3, maxit_p=600)
+    o, g, ro, rg = run_pair(mods, cfg, cfg.steps)
+    assert_parity(o, g, ro, rg)
+
+
+def test_stretched_grid_foil(mods):
+    """Geometric-progression stretched axes with the foil in the uniform patch."""
+    xn = I.stretched_axis(-3.0, 6.0, -0.8, 1.2, 1.0 / 40, 1.06)
+    yn = I.stretched_axis(-2.5, 2.5, -0.45, 0.45, 1.0 / 40, 1.06)
+    cfg = I.Config("stretched", xn, yn, Re=500.0, dt=1e-3, body=I.Body(), steps=4, maxit_p=800, perturb=0.01)
+    o, g, ro, rg = run_pair(mods, cfg, cfg.steps)
+    assert_parity(o, g, ro, rg)
+
+
+def test_cylinder_stationary(mods):
+    cfg = I.cfg2(nx=96, ny=72, steps=4, maxit_p=500)
+    o, g, ro, rg = run_pair(mods, cfg, cfg.steps)
+    assert_parity(o, g, ro, rg)
+
+
+def test_uniform_flow_fixed_point_gpu(mods):
+    cfg = I.cfg1(perturb=0.0, steps=3)
+    cfg.body = None
+    o, g, ro, rg = run_pair(mods, cfg, cfg.steps)
+    assert_parity(o, g, ro, rg)
+    assert np.abs(g.get("u") - 1.0).max() <= 1e-12 and np.abs(g.get("v")).max() <= 1e-12
+
+
+def test_check_every(mods):
+    """Convergence-test cadence R4 applied identically."""
+    cfg = I.cfg1(steps=3, check_every=4, maxit_p=2000)
+    o, g, ro, rg = run_pair(mods, cfg, cfg.steps)
+    assert_parity(o, g, ro, rg)
+
+
+def test_tight_tolerance_converged(mods):
+    """Converged solves (tol reached before maxit) on a smaller foil grid."""
+    cfg = I.cfg1(nx=64, ny=48, steps=4, omega_p=1.8, tol_p=1e-8, maxit_p=20000)
+    o, g, ro, rg = run_pair(mods, cfg, cfg.steps)
+    assert ro[0] == 0
+    assert_parity(o, g, ro, rg)
+
+
+def test_sor_batch_independent(mods):
+    """Host poll cadence does not change results (early-exit kernels)."""
+    cfg = I.cfg1(steps=2, maxit_p=700)
+    o, g, ro, rg = run_pair(mods, cfg, cfg.steps, sor_batch=3)
+    assert_parity(o, g, ro, rg)
+
+
+@pytest.mark.parametrize("P", [2, 3, 4])
+def test_loopback_slabs_bitwise(mods, P):
+    """Slab decomposition on one GPU: P slabs exchanging 2-row halos
+    by device copies give the oracle's fields bit for bit."""
+    cfg = I.cfg1(steps=3, maxit_p=800)
+    o, g, ro, rg = run_pair(mods, cfg, cfg.steps, nranks=P, loopback=True)
+    assert_parity(o, g, ro, rg)
+
+
+def test_checkpoint_restore(mods):
+    """get_fields + set_fields + set_step reproduce an uninterrupted run."""
+    O, P = mods
+    cfg = I.cfg1(steps=4, maxit_p=500)
+    u0, v0, p0 = I.initial_fields(cfg.nx, cfg.ny, cfg.perturb)
+    a = P.Solver(cfg.xn, cfg.yn, **cfg.solver_kwargs())
+    a.set_body(*cfg.body_args())
+    a.set_fields(u0, v0, p0)
+    a.step(2)
+    snap = {n: a.get(n) for n in ("u", "v", "p", "phi", "cu_prev", "cv_prev")}
+    a.step(2)
+    b = P.Solver(cfg.xn, cfg.yn, **cfg.solver_kwargs())
+    b.set_body(*cfg.body_args())
+    b.set_fields(snap["u"], snap["v"], snap["p"], phi=snap["phi"], restart=False)
+    import paper_2402_17337_b200.ibm as M
+    M.ibm_set_fields(b.ctx, (1 << 10) | (1 << 11), {10: snap["cu_prev"].ctypes.data, 11: snap["cv_prev"].ctypes.data},
+                     M.IBM_HOST)
+    b.set_step(2, True)
+    b.step(2)
+    for n in ("u", "v", "p", "phi"):
+        assert np.array_equal(a.get(n), b.get(n)), n
+
+
+def test_device_buffers_roundtrip(mods):
+    import torch
+    O, P = mods
+    cfg = I.cfg1(steps=1, maxit_p=50)
+    g = P.Solver(cfg.xn, cfg.yn, **cfg.solver_kwargs())
+    u0, v0, p0 = I.initial_fields(cfg.nx, cfg.ny, cfg.perturb)
+    g.set_fields(torch.from_numpy(u0).cuda(), torch.from_numpy(v0).cuda(), torch.from_numpy(p0).cuda())
+    assert np.array_equal(g.get("u"), u0)
+    assert torch.equal(g.get("v", device=True).cpu(), torch.from_numpy(v0))
+
+
+def test_errors_are_reported(mods):
+    O, P = mods
+    cfg = I.cfg1()
+    g = P.Solver(cfg.xn, cfg.yn, **cfg.solver_kwargs())
+    with pytest.raises(P.IBMError) as e:
+        g.set_body(0.5, 0.06, 2.4, 0.0, 0.16, 6.28)  # envelope leaves the domain
+    assert e.value.status == 2 and "envelope" in str(e.value)
+
+
+def test_nan_is_divergence(mods):
+    O, P = mods
+    cfg = I.cfg1(steps=1, maxit_p=50)
+    u0, v0, p0 = I.initial_fields(cfg.nx, cfg.ny, cfg.perturb)
+    u0[40, 50] = np.nan
+    g = P.Solver(cfg.xn, cfg.yn, **cfg.solver_kwargs())
+    g.set_body(*cfg.body_args())
+    g.set_fields(u0, v0, p0)
+    st, stats = g.step(1)
+    assert st == 3
+    o = O.Oracle(cfg.xn, cfg.yn, **cfg.solver_kwargs())
+    o.set_body(*cfg.body_args())
+    o.set_fields(u0, v0, p0)
+    so, _ = o.step(1)
+    assert so == 3
+
+
+def test_full_size_uniform_flow_fixed_point(mods):
+    """Property at BJ configs[3]'s largest size in the bench's launch
+    configuration (8192^2, tiles of 128x16, persistent grid): without a body,
+    uniform flow is an exact fixed point of every kernel."""
+    O, P = mods
+    cfg = I.cfg4(n=8192, maxit_p=20)
+    g = P.Solver(cfg.xn, cfg.yn, **cfg.solver_kwargs())
+    g.clear_body()
+    u0, v0, p0 = I.initial_fields(cfg.nx, cfg.ny)
+    g.set_fields(u0, v0, p0)
+    st, stats = g.step(1)
+    assert st == 0 and stats[0, 2] == 1
+    u = g.get("u", device=True)
+    assert float((u - 1.0).abs().max()) <= 1e-12
+    assert float(g.get("v", device=True).abs().max()) <= 1e-12
+    g.close()
+
+
+def test_full_size_loopback_invariance(mods):
+    """Property at 8192^2 with the foil: 2 slabs give bit-identical fields to 1."""
+    O, P = mods
+    import torch
+    cfg = I.cfg4(n=8192, maxit_p=30, maxit_uv=30)
+    res = []
+    for nr in (1, 2):
+        g = P.Solver(cfg.xn, cfg.yn, nranks=nr, loopback=nr > 1, **cfg.solver_kwargs())
+        g.set_body(*cfg.body_args())
+        u0, v0, p0 = I.initial_fields(cfg.nx, cfg.ny)
+        g.set_fields(u0, v0, p0)
+        st, stats = g.step(2)
+        res.append((stats.copy(), g.get("u", device=True), g.get("p", device=True)))
+        g.close()
+        del g
+        torch.cuda.empty_cache()
+    assert np.array_equal(res[0][0][:, 1:5], res[1][0][:, 1:5])
+    assert torch.equal(res[0][1], res[1][1]) and torch.equal(res[0][2], res[1][2])
