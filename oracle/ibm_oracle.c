@@ -556,6 +556,10 @@ static int step_once(orc_ctx *c)
     c->t = (double)(c->step + 1) * dt;
     orc_classify_at(c, c->t);
 
+    /* a5 masks (R16-R18) depend only on the tags, so they are built here: the
+     * predictor's pressure gradient at Fluid nodes uses open faces only (R9b) */
+    build_masks(c);
+
     /* a2: convection C^n at Fluid+Forcing nodes; first step Euler (R8) */
     convection(c, c->u, c->v, c->cu, c->cv);
     if (!c->have_hist) {
@@ -573,6 +577,7 @@ static int step_once(orc_ctx *c)
             double G = (c->p[PI_(c, i, j)] - c->p[PI_(c, i - 1, j)]) / c->hxc[i];
             double Lu = lap_at(c, 0, c->u, i, j);
             if (c->tu[id] == FLUID) {
+                if (!c->open_u[id]) G = 0.0; /* R9b: closed (solid-adjacent) face, Neumann */
                 c->rhs_u[id] = c->u[id] + dt * ((-(1.5 * C - 0.5 * Cp) - G) + halfnu * Lu);
             } else if (c->tu[id] == FORCING) {
                 double tgt = forcing_target(c, 0, c->u, c->tu, i, j, 0.0);
@@ -590,6 +595,7 @@ static int step_once(orc_ctx *c)
             double G = (c->p[PI_(c, i, j)] - c->p[PI_(c, i, j - 1)]) / c->hyc[j];
             double Lv = lap_at(c, 1, c->v, i, j);
             if (c->tv[id] == FLUID) {
+                if (!c->open_v[id]) G = 0.0; /* R9b */
                 c->rhs_v[id] = c->v[id] + dt * ((-(1.5 * C - 0.5 * Cp) - G) + halfnu * Lv);
             } else if (c->tv[id] == FORCING) {
                 double tgt = forcing_target(c, 1, c->v, c->tv, i, j, c->vb);
@@ -636,8 +642,7 @@ static int step_once(orc_ctx *c)
     /* outlet fill u*_{nx} = u*_{nx-1} (R10) */
     for (int j = 0; j < ny; ++j) c->us[UI(c, nx, j)] = c->us[UI(c, nx - 1, j)];
 
-    /* a5: masks, mass source q and Poisson rhs (R16) */
-    build_masks(c);
+    /* a5: mass source q and Poisson rhs on the masks built above (R16) */
     for (int j = 0; j < ny; ++j)
         for (int i = 0; i < nx; ++i) {
             size_t id = PI_(c, i, j);

@@ -428,6 +428,12 @@ int step_once(Ctx &c, ibm_step_stats *st) {
   }
   for (Slab &s : c.sl) launch_predictor(c, s, yb, vb);
   CK(cudaGetLastError());
+  // the fused red-black pass also updates red on the first ghost row: it needs
+  // the neighbour's right-hand side there
+  if (multi(c)) {
+    HALO((*b = s.ru, *g = &s.gu));
+    HALO((*b = s.rv, *g = &s.gv));
+  }
   CK(cudaEventRecord(c.ev[1], c.stream));
   // a4 velocity (Helmholtz) SOR, u and v jointly (R5)
   int ku = 0, sst = 0;
@@ -446,6 +452,7 @@ int step_once(Ctx &c, ibm_step_stats *st) {
   CK(cudaEventRecord(c.ev[2], c.stream));
   // a5 masks -> q, Poisson rhs; phi := 0 on inactive cells
   for (Slab &s : c.sl) launch_prhs(c, s, s.us[ures], s.vs[ures], s.phi[c.phi_cur]);
+  if (multi(c)) HALO((*b = s.bp, *g = &s.gp));
   CK(cudaEventRecord(c.ev[3], c.stream));
   // a6 Poisson SOR, warm start
   int kp = 0;

@@ -148,9 +148,9 @@ __device__ double forcing_target(const double *__restrict__ x, const uint8_t *__
 struct PredArgs {
   const double *u, *v, *p, *cup, *cvp;
   double *cu, *cv, *ru, *rv, *us, *vs, *fu, *fv;
-  const uint8_t *tu, *tv;
+  const uint8_t *tu, *tv, *pf;
   Geo gu, gv, gp;
-  BBox bu, bv;
+  BBox bu, bv, bp;
   Metric m;
   BodyNow B;
   int nx, ny, have_hist;
@@ -213,7 +213,9 @@ __global__ void k_pred_u(PredArgs A) {
   const double L = ((cE * (uE - uC) + cW * (uW - uC)) + (cN * (uN - uC) + cS * (uS - uC))) - cD * uC;
   A.cu[o] = C;
   if (t == FLUID) {
-    A.ru[o] = uC + A.dt * ((-(1.5 * C - 0.5 * Cp) - G) + A.halfnu * L);
+    // R9b: the pressure gradient acts on open faces only (closed faces are Neumann)
+    const double Gf = (A.bp.contains(i, jl) && (A.pf[gp.off(i, jl)] & PF_W)) ? 0.0 : G;
+    A.ru[o] = uC + A.dt * ((-(1.5 * C - 0.5 * Cp) - Gf) + A.halfnu * L);
     A.us[o] = uC;
     if (inbox) A.fu[o] = 0.0;
   } else {  // FORCING
@@ -272,7 +274,8 @@ __global__ void k_pred_v(PredArgs A) {
   const double L = ((cE * (vE - vC) + cW * (vW - vC)) + (cN * (vN - vC) + cS * (vS - vC))) - cD * vC;
   A.cv[o] = C;
   if (t == FLUID) {
-    A.rv[o] = vC + A.dt * ((-(1.5 * C - 0.5 * Cp) - G) + A.halfnu * L);
+    const double Gf = (A.bp.contains(i, jl) && (A.pf[gp.off(i, jl)] & PF_S)) ? 0.0 : G;
+    A.rv[o] = vC + A.dt * ((-(1.5 * C - 0.5 * Cp) - Gf) + A.halfnu * L);
     A.vs[o] = vC;
     if (inbox) A.fv[o] = 0.0;
   } else {
@@ -665,9 +668,9 @@ void launch_predictor(const Ctx &c, const Slab &s, double yb, double vb) {
   PredArgs A;
   A.u = s.u; A.v = s.v; A.p = s.p; A.cup = s.cup; A.cvp = s.cvp;
   A.cu = s.cu; A.cv = s.cv; A.ru = s.ru; A.rv = s.rv; A.us = s.us[0]; A.vs = s.vs[0]; A.fu = s.fu; A.fv = s.fv;
-  A.tu = s.tu; A.tv = s.tv;
+  A.tu = s.tu; A.tv = s.tv; A.pf = s.pf;
   A.gu = s.gu; A.gv = s.gv; A.gp = s.gp;
-  A.bu = s.bu; A.bv = s.bv;
+  A.bu = s.bu; A.bv = s.bv; A.bp = s.bpb;
   A.m = c.m;
   A.B.a = c.body.a; A.B.b = c.body.b; A.B.xb = c.body.x0; A.B.yb = yb; A.B.vb = vb;
   A.nx = c.nx; A.ny = c.ny; A.have_hist = c.have_hist;

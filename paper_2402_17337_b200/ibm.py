@@ -65,6 +65,9 @@ def lib():
     """Loads the in-tree CUDA library; raises if it has not been built."""
     global _lib
     if _lib is None:
+        # torch first: its bundled libnccl.so.2 must be the one the process loads
+        # (libibm_b200.so links NCCL by soname and reuses whichever is loaded)
+        import torch  # noqa: F401
         if not os.path.exists(LIB_PATH):
             raise ImportError("libibm_b200.so not built: run __graft_entry__.build() "
                               "(there is no CPU fallback)")
@@ -272,7 +275,9 @@ class Solver:
         the step counter and AB2 history are reset (ibm_set_step(0, 0))."""
         keep, ptrs, mask, where = [], {}, 0, None
         if restart and phi is None:
-            phi = np.zeros(self.shape("phi"))
+            on_dev = any(hasattr(a, "data_ptr") for a in (u, v, p))
+            phi = (self.torch.zeros(self.shape("phi"), dtype=self.torch.float64, device=self.device)
+                   if on_dev else np.zeros(self.shape("phi")))
         for name, arr in (("u", u), ("v", v), ("p", p), ("phi", phi)):
             if arr is None:
                 continue
