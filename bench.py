@@ -1,0 +1,350 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 IBM hot path (one JSON line on rank 0).
+
+Workload (BASELINE.json configs[3], input-scaling sweep, largest size that is
+HBM-bound): plunging elliptic foil (t/c 0.12, Re 500, k 2 pi, h 0.16; P:33,
+P:150) on an N x N uniform staggered grid over the paper's domain
+[-7.5,24]x[-12.5,12.5], N = 8192 (dx ~ 0.0038 ~ the paper's 0.004), dt
+1e-4, impulsive start, SOR omega 1.5/1.2, tol 1e-6/1e-8, maxit 10000/1000
+(S:327).  A "step" is one time step of the whole hot path (classify,
+predictor + forcing, velocity SOR, Poisson rhs, Poisson SOR to tol or maxit,
+projection, forces) -- ibm_step(ctx, 1).
+
+metric: Poisson+stencil grid-point updates/s
+  = sum over steps of [it_p*Np + it_uv*(Nu+Nv) + 2*(Nu+Nv) + 2*Np] / time
+  (SOR node updates + one node update per stencil pass: predictor, Poisson
+  rhs, correction) -- DESIGN.md §7.  ms_per_step is reported beside it.
+
+Multi-GPU (torchrun, N>1): the same grid split into N slabs along y (strong
+scaling), NCCL halos + residual all-reduce; time = max over ranks.
+--impl reference: the CPU oracle (oracle/) timed as it stands on the host
+cores, on a bounded sample of the same workload (there is no reference
+implementation to install: the paper ships no code).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import ibm_inputs as I  # noqa: E402
+
+METRIC = "Poisson+stencil grid-point updates/s"
+UNIT = "grid-point updates/s"
+BYTES_PER_POISSON_UPDATE = 24  # phi read + b read + phi write, fp64
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=8192, help="grid N x N on the paper domain")
+    ap.add_argument("--maxit-p", type=int, default=10000)
+    ap.add_argument("--maxit-uv", type=int, default=1000)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--cpu-sample-n", type=int, default=0, help="oracle sample grid (0 = auto)")
+    return ap.parse_args()
+
+
+def node_counts(nx, ny):
+    return (nx + 1) * ny, nx * (ny + 1), nx * ny
+
+
+def updates_for(stats, nx, ny):
+    Nu, Nv, Np = node_counts(nx, ny)
+    it_uv, it_p = stats[:, 1].sum(), stats[:, 2].sum()
+    n = stats.shape[0]
+    return float(it_p * Np + it_uv * (Nu + Nv) + n * (2 * (Nu + Nv) + 2 * Np))
+
+
+# ---------------------------------------------------------------- clocks sampler
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index, enabled=True):
+        self.index, self.enabled, self.rows, self.proc = index, enabled, [], None
+
+    def start(self):
+        if not self.enabled:
+            return
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.th.join(timeout=2)
+        rows = [r for r in self.rows if len(r) >= 8]
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[4 + k].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------- CPU oracle sample
+def mem_available_gb():
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable"):
+                return int(line.split()[1]) / 1e6
+    except Exception:
+        pass
+    return 8.0
+
+
+def oracle_sample_n(n_req, requested):
+    if requested:
+        return requested
+    # oracle: ~30 fp64 full arrays + SOR coefficient temporaries ~ 330 B/cell
+    avail = mem_available_gb() * 1e9 * 0.4
+    n = n_req
+    while n > 512 and 330.0 * n * n > avail:
+        n //= 2
+    return n
+
+
+def run_oracle_steps(n, steps, maxit_p, maxit_uv):
+    """One oracle instance on the N x N workload; each step capped at maxit
+    iterations (a bounded sample).  Returns (updates/s, seconds, stats, n)."""
+    from oracle import oracle as O
+    O.build()
+    cfg = I.cfg4(n=n, maxit_p=maxit_p, maxit_uv=maxit_uv)
+    o = O.Oracle(cfg.xn, cfg.yn, **cfg.solver_kwargs())
+    o.set_body(*cfg.body_args())
+    o.set_fields(*I.initial_fields(cfg.nx, cfg.ny))
+    per = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        st, stats = o.step(1)
+        per.append((time.perf_counter() - t0, stats))
+    secs = sum(p[0] for p in per)
+    allstats = np.concatenate([p[1] for p in per])
+    return updates_for(allstats, cfg.nx, cfg.ny) / secs, secs, allstats, per
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(args):
+    n = oracle_sample_n(args.n, args.cpu_sample_n)
+    v, secs, stats, _ = run_oracle_steps(n, 1, 3, 3)
+    return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": "1 time step of the %dx%d foil workload with SOR capped at 3+3 iterations "
+                      "(%.1f s, single-threaded plain-C oracle, %s)" % (n, n, secs, cpu_model())}
+
+
+# ---------------------------------------------------------------- reference arm = oracle
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    n = oracle_sample_n(args.n, args.cpu_sample_n)
+    maxit = 3
+    total = args.warmup + args.steps
+    v, secs, stats, per = run_oracle_steps(n, total, maxit, maxit)
+    timed = per[args.warmup:]
+    tsec = sum(p[0] for p in timed)
+    tstats = np.concatenate([p[1] for p in timed])
+    cfgd = I.cfg4(n=n)
+    value = updates_for(tstats, cfgd.nx, cfgd.ny) / tsec
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tsec / max(args.steps, 1),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": "cfg4-foil-%dx%d" % (args.n, args.n), "oracle_sample_n": n,
+                       "maxit_p": maxit, "maxit_uv": maxit},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": "%d oracle time steps of the %dx%d foil workload, SOR capped at %d+%d "
+                                       "iterations per step (%s)" % (args.steps, n, n, maxit, maxit, cpu_model())},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- B200 arm
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2402_17337_b200 as P
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    nccl_id = None
+    if world > 1:
+        obj = [P.ibm_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+
+    cfg = I.cfg4(n=args.n, maxit_p=args.maxit_p, maxit_uv=args.maxit_uv)
+    g = P.Solver(cfg.xn, cfg.yn, device=local, rank=rank, nranks=world, nccl_id=nccl_id, **cfg.solver_kwargs())
+    g.set_body(*cfg.body_args())
+    u0, v0, p0 = I.initial_fields(cfg.nx, cfg.ny)
+    j0, j1 = g.rows
+    last = j1 == cfg.ny
+    g.set_fields(u0[j0:j1], v0[j0:j1 + (1 if last else 0)], p0[j0:j1])
+    stream = g.stream
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+
+    # warm-up
+    if args.warmup:
+        g.step(args.warmup)
+    barrier()
+    clocks = Clocks(local, enabled=(rank == 0 and not args.no_clocks))
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    st, stats = g.step(args.steps)
+    e1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    t_ms = e0.elapsed_time(e1)
+    raw = g.last_stats
+    launches = int(sum(raw[k].launches for k in range(args.steps)))
+    psor_ms = float(sum(raw[k].ms[3] for k in range(args.steps)))
+    uvsor_ms = float(sum(raw[k].ms[1] for k in range(args.steps)))
+    if world > 1:
+        t = torch.tensor([t_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_ms = float(t.item())
+    updates = updates_for(stats, cfg.nx, cfg.ny)
+    value = updates / (t_ms / 1e3)
+
+    # roofline of the dominant kernel (Poisson red-black SOR pass): algorithmic
+    # bytes per launch = 24 B x this rank's p cells; duration from CUDA events
+    # bracketing the Poisson loop on the launch stream, / iterations
+    Np_local = cfg.nx * (j1 - j0)
+    it_p = float(stats[:, 2].sum())
+    avg_launch_s = (psor_ms / 1e3) / max(it_p, 1.0)
+    achieved = BYTES_PER_POISSON_UPDATE * Np_local / avg_launch_s / 1e9
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        peak, peak_src = float(peaks["hbm_gbs"]), "measured"
+    except Exception:
+        peak, peak_src = 6650.0, "fallback"
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        traffic = prof.get("k_sor_poisson", {}).get("dram_bytes_per_cell", None)
+        if traffic is not None:
+            traffic = float(traffic) * Np_local
+    except Exception:
+        pass
+
+    # end to end through the C ABI with host buffers: per step the state comes
+    # from pinned host memory (H2D) and the step's fields go back (D2H)
+    e2e = None
+    if not args.no_e2e:
+        shapes = {n: g.shape(n) for n in ("u", "v", "p")}
+        host = {n: torch.empty(shapes[n], dtype=torch.float64, pin_memory=True) for n in shapes}
+        for n in host:
+            host[n].copy_(g.get(n, device=True))
+        import paper_2402_17337_b200.ibm as M
+        ptrs = {M.FIELD_BITS[n]: host[n].data_ptr() for n in host}
+        mask = sum(1 << M.FIELD_BITS[n] for n in host)
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        estats = []
+        for _ in range(args.steps):
+            M.ibm_set_fields(g.ctx, mask, ptrs, M.IBM_HOST)
+            s2, st2 = g.step(1)
+            estats.append(st2)
+            M.ibm_get_fields(g.ctx, mask, ptrs, M.IBM_HOST)
+        f1.record(stream)
+        barrier()
+        te = f0.elapsed_time(f1)
+        if world > 1:
+            t = torch.tensor([te], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = float(t.item())
+        nbytes = sum(host[n].numel() * 8 for n in host)
+        e2e = {"value": updates_for(np.concatenate(estats), cfg.nx, cfg.ny) / (te / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": te / args.steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "cfg4-foil-%dx%d" % (cfg.nx, cfg.ny), "nx": cfg.nx, "ny": cfg.ny,
+                       "domain": list(I.PAPER_DOMAIN), "Re": cfg.Re, "dt": cfg.dt, "omega_p": cfg.omega_p,
+                       "tol_p": cfg.tol_p, "maxit_p": cfg.maxit_p, "omega_uv": cfg.omega_uv,
+                       "tol_uv": cfg.tol_uv, "maxit_uv": cfg.maxit_uv, "body": "foil a=0.5 b=0.06 h=0.16 k=2pi",
+                       "l2": "inputs larger than L2 (%.1f GB workspace, 126 MB L2)" % (g.ws.numel() / 1e9),
+                       "parallelism": "slab%d" % world},
+            "it_p": stats[:, 2].tolist(), "it_uv": stats[:, 1].tolist(),
+            "poisson_ms_per_iteration": 1e3 * avg_launch_s, "uv_sor_ms": uvsor_ms / args.steps,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "k_sor<0> (fused red-black Poisson pass)",
+                         "bytes_per_launch": BYTES_PER_POISSON_UPDATE * Np_local, "peak_source": peak_src},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    g.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

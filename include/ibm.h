@@ -97,6 +97,8 @@ typedef struct {
     double cd, cl;              /* force coefficients of this step */
     float ms[6];                /* device ms: classify+predictor, uv-SOR, rhs, p-SOR, correct, forces */
     int status;                 /* IBM_OK / IBM_WARN_NOCONV / IBM_ERR_DIVERGED */
+    int launches;               /* CUDA kernels this library launched for the step (incl.
+                                   early-exit SOR iterations past convergence) */
 } ibm_step_stats;
 
 /* Bytes of device workspace ibm_init needs for this configuration. */

@@ -377,11 +377,13 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
           a.f[0].xin = s.phi[in]; a.f[0].xout = s.phi[out];
         }
         launch_sor_iteration(a, c.stream, grids[r]);
+        ++c.launches;
       }
       if (mult) {
         if (!c.loopback)
           NK(ncclAllReduce(c.rho_bits + kk, c.rho_bits + kk, 1, ncclUint64, ncclMax, (ncclComm_t)c.nccl, c.stream));
         launch_sor_check(c.ctl, c.rho_bits, kk, maxit, cfg.check_every, tol, c.stream);
+        ++c.launches;
       }
     }
     CK(cudaGetLastError());
@@ -413,12 +415,13 @@ int step_once(Ctx &c, ibm_step_stats *st) {
   if (c.body.has) plunge(t1, c.body.hbar, c.body.k, &disp, &vb);
   const double yb = c.body.y0 + disp;
   int status = IBM_OK;
+  c.launches = 0;
   CK(cudaEventRecord(c.ev[0], c.stream));
   // a1 classification at t^{n+1} (R15) + Poisson masks
   if (c.body.has)
     for (Slab &s : c.sl) {
-      launch_classify(c, s, yb);
-      launch_pflags(c, s);
+      c.launches += launch_classify(c, s, yb);
+      c.launches += launch_pflags(c, s);
     }
   // N1 halos of u^n, v^n, p^n, then a2/a3 predictor
   if (multi(c)) {
@@ -426,7 +429,7 @@ int step_once(Ctx &c, ibm_step_stats *st) {
     HALO((*b = s.v, *g = &s.gv));
     HALO((*b = s.p, *g = &s.gp));
   }
-  for (Slab &s : c.sl) launch_predictor(c, s, yb, vb);
+  for (Slab &s : c.sl) c.launches += launch_predictor(c, s, yb, vb);
   CK(cudaGetLastError());
   // the fused red-black pass also updates red on the first ghost row: it needs
   // the neighbour's right-hand side there
@@ -444,14 +447,14 @@ int step_once(Ctx &c, ibm_step_stats *st) {
   if (sst == 3) { c.err = "velocity SOR residual is NaN at step " + std::to_string(c.step + 1); return IBM_ERR_DIVERGED; }
   if (sst == 1) status = IBM_WARN_NOCONV;
   const int ures = ku & 1;
-  for (Slab &s : c.sl) launch_outlet_fill(c, s, s.us[ures]);
+  for (Slab &s : c.sl) c.launches += launch_outlet_fill(c, s, s.us[ures]);
   if (multi(c)) {
     HALO((*b = s.us[ures], *g = &s.gu));
     HALO((*b = s.vs[ures], *g = &s.gv));
   }
   CK(cudaEventRecord(c.ev[2], c.stream));
   // a5 masks -> q, Poisson rhs; phi := 0 on inactive cells
-  for (Slab &s : c.sl) launch_prhs(c, s, s.us[ures], s.vs[ures], s.phi[c.phi_cur]);
+  for (Slab &s : c.sl) c.launches += launch_prhs(c, s, s.us[ures], s.vs[ures], s.phi[c.phi_cur]);
   if (multi(c)) HALO((*b = s.bp, *g = &s.gp));
   CK(cudaEventRecord(c.ev[3], c.stream));
   // a6 Poisson SOR, warm start
@@ -467,7 +470,7 @@ int step_once(Ctx &c, ibm_step_stats *st) {
   CK(cudaEventRecord(c.ev[4], c.stream));
   // a7 projection
   CK(cudaMemsetAsync(c.nanflag, 0, sizeof(int), c.stream));
-  for (Slab &s : c.sl) launch_correct(c, s, s.us[ures], s.vs[ures], s.phi[c.phi_cur]);
+  for (Slab &s : c.sl) c.launches += launch_correct(c, s, s.us[ures], s.vs[ures], s.phi[c.phi_cur]);
   CK(cudaEventRecord(c.ev[5], c.stream));
   // history rotation
   for (Slab &s : c.sl) {
@@ -476,7 +479,7 @@ int step_once(Ctx &c, ibm_step_stats *st) {
   }
   c.have_hist = 1;
   // a8 forces
-  for (Slab &s : c.sl) launch_forces(c, s);
+  for (Slab &s : c.sl) c.launches += launch_forces(c, s);
   CK(cudaGetLastError());
   CK(cudaEventRecord(c.ev[6], c.stream));
   double sums[4];
@@ -501,6 +504,7 @@ int step_once(Ctx &c, ibm_step_stats *st) {
     st->ms[3] = ev_ms(c, 3, 4);
     st->ms[4] = ev_ms(c, 4, 5);
     st->ms[5] = ev_ms(c, 5, 6);
+    st->launches = c.launches;
   }
   if (*c.h_nan) {
     c.err = "non-finite field after correction at step " + std::to_string(c.step);

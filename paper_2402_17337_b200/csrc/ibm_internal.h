@@ -114,23 +114,24 @@ struct Ctx {
   double Mx, My;
   double last_t, last_cd, last_cl;
   int hint_uv, hint_p;
+  int launches;     // kernels launched in the current step
   cudaEvent_t ev[8];
   void *nccl;      // ncclComm_t when nranks > 1 and !loopback
   std::string err;
 };
 
 // kernel launchers (kernels.cu)
-void launch_classify(const Ctx &c, const Slab &s, double yb);
-void launch_pflags(const Ctx &c, const Slab &s);
-void launch_predictor(const Ctx &c, const Slab &s, double yb, double vb);
+int launch_classify(const Ctx &c, const Slab &s, double yb);
+int launch_pflags(const Ctx &c, const Slab &s);
+int launch_predictor(const Ctx &c, const Slab &s, double yb, double vb);
 int sor_grid(const SorArgs &a);
 void launch_sor_iteration(const SorArgs &a, cudaStream_t st, int grid);
 void launch_sor_check(SorCtl *ctl, const unsigned long long *rho_bits, int k, int maxit, int check_every,
                       double tol, cudaStream_t st);
-void launch_outlet_fill(const Ctx &c, const Slab &s, double *us);
-void launch_prhs(const Ctx &c, const Slab &s, const double *us, const double *vs, double *phi_start);
-void launch_correct(const Ctx &c, const Slab &s, const double *us, const double *vs, const double *phi);
-void launch_forces(const Ctx &c, const Slab &s);
+int launch_outlet_fill(const Ctx &c, const Slab &s, double *us);
+int launch_prhs(const Ctx &c, const Slab &s, const double *us, const double *vs, double *phi_start);
+int launch_correct(const Ctx &c, const Slab &s, const double *us, const double *vs, const double *phi);
+int launch_forces(const Ctx &c, const Slab &s);
 void launch_fill(double *p, const Geo &g, double val, cudaStream_t st);
 
 }  // namespace ibm

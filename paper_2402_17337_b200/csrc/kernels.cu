@@ -633,7 +633,8 @@ __global__ void k_fill(double *__restrict__ p, Geo g, double val) {
 // ================================================================ launchers
 static dim3 grid2(int ni, int nj, dim3 b) { return dim3((ni + b.x - 1) / b.x, (nj + b.y - 1) / b.y); }
 
-void launch_classify(const Ctx &c, const Slab &s, double yb) {
+int launch_classify(const Ctx &c, const Slab &s, double yb) {
+  int n = 0;
   const Body &B = c.body;
   struct F {
     uint8_t *t;
@@ -649,22 +650,25 @@ void launch_classify(const Ctx &c, const Slab &s, double yb) {
     dim3 blk(32, 8);
     k_classify<<<grid2(box.i1 - box.i0, box.j1 - box.j0, blk), blk, 0, c.stream>>>(f.t, *f.g, box, f.xs, f.ys, B.a,
                                                                                      B.b, B.x0, yb);
+    ++n;
   }
+  return n;
 }
 
-void launch_pflags(const Ctx &c, const Slab &s) {
-  if (s.bpb.empty()) return;
+int launch_pflags(const Ctx &c, const Slab &s) {
+  if (s.bpb.empty()) return 0;
   // flags are needed on the owned rows and one ghost row each side
   BBox box = s.bpb;
   box.j0 = box.j0 < -1 ? -1 : box.j0;
   box.j1 = box.j1 > s.gp.nj + 1 ? s.gp.nj + 1 : box.j1;
-  if (box.empty()) return;
+  if (box.empty()) return 0;
   dim3 blk(32, 8);
   k_pflags<<<grid2(box.i1 - box.i0, box.j1 - box.j0, blk), blk, 0, c.stream>>>(s.pf, s.tp, s.tu, s.tv, s.gp, s.gu,
                                                                                 s.gv, box, c.m, c.nx, c.ny);
+  return 1;
 }
 
-void launch_predictor(const Ctx &c, const Slab &s, double yb, double vb) {
+int launch_predictor(const Ctx &c, const Slab &s, double yb, double vb) {
   PredArgs A;
   A.u = s.u; A.v = s.v; A.p = s.p; A.cup = s.cup; A.cvp = s.cvp;
   A.cu = s.cu; A.cv = s.cv; A.ru = s.ru; A.rv = s.rv; A.us = s.us[0]; A.vs = s.vs[0]; A.fu = s.fu; A.fv = s.fv;
@@ -680,6 +684,7 @@ void launch_predictor(const Ctx &c, const Slab &s, double yb, double vb) {
   dim3 blk(128, 2);
   k_pred_u<<<grid2(s.gu.ni, s.gu.nj, blk), blk, 0, c.stream>>>(A);
   k_pred_v<<<grid2(s.gv.ni, s.gv.nj, blk), blk, 0, c.stream>>>(A);
+  return 2;
 }
 
 static int g_sor_blocks[2] = {0, 0};
@@ -716,23 +721,26 @@ void launch_sor_check(SorCtl *ctl, const unsigned long long *rho_bits, int k, in
   k_sor_check<<<1, 1, 0, s>>>(ctl, rho_bits, k, maxit, check_every, tol);
 }
 
-void launch_outlet_fill(const Ctx &c, const Slab &s, double *us) {
+int launch_outlet_fill(const Ctx &c, const Slab &s, double *us) {
   k_outlet_fill<<<(s.gu.nj + 127) / 128, 128, 0, c.stream>>>(us, s.gu, c.nx);
+  return 1;
 }
 
-void launch_prhs(const Ctx &c, const Slab &s, const double *us, const double *vs, double *phi_start) {
+int launch_prhs(const Ctx &c, const Slab &s, const double *us, const double *vs, double *phi_start) {
   dim3 blk(128, 2);
   k_prhs<<<grid2(s.gp.ni, s.gp.nj, blk), blk, 0, c.stream>>>(us, vs, s.bp, s.q, phi_start, s.pf, s.gp, s.gu, s.gv,
                                                              s.bpb, c.m, c.nx, c.ny, c.cfg.dt);
+  return 1;
 }
 
-void launch_correct(const Ctx &c, const Slab &s, const double *us, const double *vs, const double *phi) {
+int launch_correct(const Ctx &c, const Slab &s, const double *us, const double *vs, const double *phi) {
   dim3 blk(128, 2);
   k_correct_u<<<grid2(s.gu.ni, s.gu.nj, blk), blk, 0, c.stream>>>(s.u, us, phi, s.pf, s.gu, s.gp, s.bpb, c.m, c.nx,
                                                                   c.cfg.dt, c.nanflag);
   k_correct_v<<<grid2(s.gv.ni, s.gv.nj, blk), blk, 0, c.stream>>>(s.v, vs, phi, s.pf, s.gv, s.gp, s.bpb, c.m, c.ny,
                                                                   c.cfg.dt, c.nanflag);
   k_correct_p<<<grid2(s.gp.ni, s.gp.nj, blk), blk, 0, c.stream>>>(s.p, phi, s.pf, s.gp, s.bpb, c.nanflag);
+  return 3;
 }
 
 void launch_fill(double *p, const Geo &g, double val, cudaStream_t st) {
@@ -740,9 +748,10 @@ void launch_fill(double *p, const Geo &g, double val, cudaStream_t st) {
   k_fill<<<grid2(g.ni, g.nj, blk), blk, 0, st>>>(p, g, val);
 }
 
-void launch_forces(const Ctx &c, const Slab &s) {
+int launch_forces(const Ctx &c, const Slab &s) {
   k_forces<<<1, 512, 0, c.stream>>>(s.u, s.v, s.fu, s.fv, s.tu, s.tv, s.gu, s.gv, s.bu, s.bv, c.m, c.nx, c.ny,
                                      s.red);
+  return 1;
 }
 
 }  // namespace ibm

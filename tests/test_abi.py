@@ -61,16 +61,16 @@ def test_struct_layout_matches_header(ibm, tmp_path):
     import subprocess
     probe = tmp_path / "probe.c"
     probe.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "ibm.h"\n'
-                     'int main(){printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(ibm_config),'
+                     'int main(){printf("%zu %zu %zu %zu %zu %zu %zu\\n", sizeof(ibm_config),'
                      ' offsetof(ibm_config, loopback), offsetof(ibm_config, nccl_id),'
-                     ' sizeof(ibm_step_stats), offsetof(ibm_step_stats, status), offsetof(ibm_step_stats, ms));'
+                     ' sizeof(ibm_step_stats), offsetof(ibm_step_stats, status), offsetof(ibm_step_stats, ms), offsetof(ibm_step_stats, launches));'
                      'return 0;}\n')
     exe = tmp_path / "probe"
     subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(probe), "-o", str(exe)])
     vals = [int(x) for x in subprocess.check_output([str(exe)]).split()]
     assert vals == [C.sizeof(ibm.ibm_config), ibm.ibm_config.loopback.offset, ibm.ibm_config.nccl_id.offset,
                     C.sizeof(ibm.ibm_step_stats), ibm.ibm_step_stats.status.offset,
-                    ibm.ibm_step_stats.ms.offset]
+                    ibm.ibm_step_stats.ms.offset, ibm.ibm_step_stats.launches.offset]
 
 
 def test_workspace_size_scales(ibm):
