@@ -12,6 +12,7 @@
 #include <new>
 #include <string>
 
+#include <cudaTypedefs.h>
 #include <nccl.h>
 
 #include "ibm_internal.h"
@@ -218,6 +219,46 @@ BBox box_for(const std::vector<double> &xs, const std::vector<double> &ys, doubl
   return b;
 }
 
+// ---------------------------------------------------------------- TMA descriptors
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D map over a family array incl. its ghost rows: dim0 = columns, dim1 = stored
+// rows; elements outside are zero-filled by the TMA unit
+bool make_map(CUtensorMap *m, double *base, const Geo &g, int box_h) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)g.ni, (cuuint64_t)(g.nj + 2 * kGhost)};
+  cuuint64_t strides[1] = {(cuuint64_t)g.pitch * sizeof(double)};
+  cuuint32_t box[2] = {(cuuint32_t)kSorBoxW, (cuuint32_t)box_h};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool make_maps(Slab &s) {
+  bool ok = true;
+  for (int q = 0; q < 2; ++q) {
+    ok = ok && make_map(&s.tm_phi[q], s.phi[q], s.gp, kSorBoxHx);
+    ok = ok && make_map(&s.tm_us[q], s.us[q], s.gu, kSorBoxHx);
+    ok = ok && make_map(&s.tm_vs[q], s.vs[q], s.gv, kSorBoxHx);
+  }
+  ok = ok && make_map(&s.tm_bp, s.bp, s.gp, kSorBoxHb);
+  ok = ok && make_map(&s.tm_ru, s.ru, s.gu, kSorBoxHb);
+  ok = ok && make_map(&s.tm_rv, s.rv, s.gv, kSorBoxHb);
+  return ok;
+}
+
 // ---------------------------------------------------------------- halos and reductions
 // exchange 2 ghost rows of one family buffer (selected per slab by `pick`)
 template <class Pick>
@@ -371,10 +412,10 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
         SorArgs &a = args[r];
         a.k = kk;
         if (helm) {
-          a.f[0].xin = s.us[in]; a.f[0].xout = s.us[out];
-          a.f[1].xin = s.vs[in]; a.f[1].xout = s.vs[out];
+          a.f[0].xin = s.us[in]; a.f[0].xout = s.us[out]; a.f[0].tmx = s.tm_us[in]; a.f[0].tmb = s.tm_ru;
+          a.f[1].xin = s.vs[in]; a.f[1].xout = s.vs[out]; a.f[1].tmx = s.tm_vs[in]; a.f[1].tmb = s.tm_rv;
         } else {
-          a.f[0].xin = s.phi[in]; a.f[0].xout = s.phi[out];
+          a.f[0].xin = s.phi[in]; a.f[0].xout = s.phi[out]; a.f[0].tmx = s.tm_phi[in]; a.f[0].tmb = s.tm_bp;
         }
         launch_sor_iteration(a, c.stream, grids[r]);
         ++c.launches;
@@ -585,6 +626,11 @@ int ibm_init(const ibm_config *cfg, void *d_workspace, size_t bytes, void *cuda_
     return fail(IBM_ERR_ARG);
   }
   carve(c, (char *)d_workspace);
+  for (Slab &s : c.sl)
+    if (!make_maps(s)) {
+      c.err = "cuTensorMapEncodeTiled unavailable or failed";
+      return fail(IBM_ERR_CUDA);
+    }
   if (cudaHostAlloc((void **)&c.h_ctl, 2 * sizeof(SorCtl), cudaHostAllocDefault) != cudaSuccess ||
       cudaHostAlloc((void **)&c.h_red, 4 * sizeof(double) * c.sl.size(), cudaHostAllocDefault) != cudaSuccess ||
       cudaHostAlloc((void **)&c.h_nan, sizeof(int), cudaHostAllocDefault) != cudaSuccess) {

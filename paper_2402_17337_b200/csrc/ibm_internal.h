@@ -10,6 +10,7 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>  // CUtensorMap (TMA descriptors); no libcuda link
 #include <cuda_runtime.h>
 
 #include "../../include/ibm.h"
@@ -40,6 +41,8 @@ struct BBox {  // half-open node-index box: global columns, LOCAL rows
 
 // One family of one red-black SOR system (Poisson: phi; Helmholtz: u* or v*).
 struct SorFam {
+  CUtensorMap tmx;      // TMA map of the input iterate (box SW x SH)
+  CUtensorMap tmb;      // TMA map of the right-hand side (box SW x SH-2)
   const double *xin;
   double *xout;
   const double *b;
@@ -92,6 +95,8 @@ struct Slab {
   uint8_t *tu, *tv, *tp, *pf;
   BBox bu, bv, bpb;  // body envelope boxes (local rows incl. ghosts), empty without body
   double *red;       // force partial sums [4]
+  // TMA descriptors of the SOR operands (built once at init)
+  CUtensorMap tm_phi[2], tm_bp, tm_us[2], tm_ru, tm_vs[2], tm_rv;
 };
 
 struct Ctx {
@@ -125,6 +130,8 @@ int launch_classify(const Ctx &c, const Slab &s, double yb);
 int launch_pflags(const Ctx &c, const Slab &s);
 int launch_predictor(const Ctx &c, const Slab &s, double yb, double vb);
 int sor_grid(const SorArgs &a);
+// TMA box of the SOR tile (x) and of its right-hand side (b)
+constexpr int kSorBoxW = 132, kSorBoxHx = 20, kSorBoxHb = 18;
 void launch_sor_iteration(const SorArgs &a, cudaStream_t st, int grid);
 void launch_sor_check(SorCtl *ctl, const unsigned long long *rho_bits, int k, int maxit, int check_every,
                       double tol, cudaStream_t st);
