@@ -13,7 +13,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libibm_b200.so")
-SOURCES = ["kernels.cu", "api.cu"]
+SOURCES = ["kernels.cu", "sor.cu", "api.cu"]
 HEADERS = ["ibm_internal.h", os.path.join("..", "..", "include", "ibm.h")]
 
 NVCC_FLAGS = [

@@ -376,8 +376,8 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
       f.g = g; f.b = b; f.flag = flag; f.box = box;
       f.cE = cE; f.cW = cW; f.cD = cD; f.cN = cN; f.cS = cS;
       f.ui0 = ui0; f.ui1 = ui1; f.uj0 = uj0; f.uj1 = uj1;
-      f.tiles_x = (g.ni + 127) / 128;
-      f.tiles_y = (g.nj + 15) / 16;
+      f.tiles_x = (g.ni + kSorTileX - 1) / kSorTileX;
+      f.tiles_y = (g.nj + kSorTileY - 1) / kSorTileY;
     };
     const Metric &m = c.m;
     if (helm) {

@@ -287,261 +287,6 @@ __global__ void k_pred_v(PredArgs A) {
   }
 }
 
-// ---------------------------------------------------------------- a4/a6: red-black SOR
-// One launch = one full red-black iteration (R1-R3), fused in one HBM
-// pass.  Persistent CTAs walk tiles of TX x TY owned nodes; for each tile one
-// thread issues two TMA box loads (x with a 2-node halo, b with a 1-node halo)
-// into a double-buffered shared-memory stage armed on an mbarrier, so the next
-// tile streams in while the current one is computed.  Out-of-bounds box
-// elements are zero-filled by the TMA unit -- exactly the oracle's "0 outside
-// the family" reads.  Red is updated on the tile plus its 1-node ring
-// (recomputed redundantly, bit-identical to the neighbour's own update), then
-// black on the tile, then the whole tile is stored to the other ping-pong
-// buffer.  The scaled residual |gs - x_old| is max-reduced on its uint64 bit
-// pattern (exact, NaN-propagating): warp shuffle -> block -> atomicMax; the last
-// CTA takes the convergence decision for iteration k on the device.
-constexpr int TX = 128, TY = 16, SW = TX + 4, SH = TY + 4, NT = 256;
-constexpr unsigned kBytesX = SW * SH * 8, kBytesB = SW * (SH - 2) * 8;
-static_assert(SW == kSorBoxW && SH == kSorBoxHx && SH - 2 == kSorBoxHb, "TMA boxes must match the tile");
-
-struct __align__(128) SorStage {
-  double x[SH][SW];
-  double b[SH - 2][SW];  // rows j0-1 .. j0+TY
-};
-struct SorAux {
-  double cE[SW], cW[SW], cD[SW], cN[SH], cS[SH];
-  uint8_t f[SH][SW];
-  unsigned long long bar[2];
-  unsigned long long wmax[NT / 32];
-};
-constexpr size_t kSorSmem = 2 * sizeof(SorStage) + sizeof(SorAux) + 128;
-
-__device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) {
-  return a > b ? a : b;
-}
-__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(unsigned long long *bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t phase) {
-  uint32_t done = 0;
-  do {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(phase)
-        : "memory");
-  } while (!done);
-}
-__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1,
-                                            unsigned long long *bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ const SorFam &fam_of(const SorArgs &A, int t, int nt0, int &tt) {
-  if (t < nt0) {
-    tt = t;
-    return A.f[0];
-  }
-  tt = t - nt0;
-  return A.f[1];
-}
-
-// one thread: arm the stage barrier and issue the two box loads of tile t
-__device__ __forceinline__ void sor_issue(const SorArgs &A, int t, int nt0, SorStage &S, unsigned long long *bar) {
-  int tt;
-  const SorFam &F = fam_of(A, t, nt0, tt);
-  const int i0 = (tt % F.tiles_x) * TX, j0 = (tt / F.tiles_x) * TY;
-  mbar_expect_tx(bar, kBytesX + kBytesB);
-  // storage row of local row jl is jl + kGhost
-  tma_load_2d(&S.x[0][0], &F.tmx, i0 - 2, j0 - 2 + kGhost, bar);
-  tma_load_2d(&S.b[0][0], &F.tmb, i0 - 2, j0 - 1 + kGhost, bar);
-}
-
-template <int HELM>
-__device__ __forceinline__ void sor_tile(const SorFam &F, SorStage &S, SorAux &X, int tt, const SorArgs &A,
-                                         unsigned long long &tmax) {
-  const int i0 = (tt % F.tiles_x) * TX, j0 = (tt / F.tiles_x) * TY;
-  const Geo g = F.g;
-  const bool hasf = !F.box.empty() && (i0 - 2 < F.box.i1) && (i0 + TX + 2 > F.box.i0) && (j0 - 1 < F.box.j1) &&
-                    (j0 + TY + 1 > F.box.j0);
-  for (int c = threadIdx.x; c < SW; c += NT) {
-    const int gi = i0 - 2 + c;
-    const bool ok = gi >= 0 && gi < g.ni;
-    X.cE[c] = ok ? __ldg(F.cE + gi) : 0.0;
-    X.cW[c] = ok ? __ldg(F.cW + gi) : 0.0;
-    X.cD[c] = ok ? __ldg(F.cD + gi) : 0.0;
-  }
-  for (int r = threadIdx.x; r < SH; r += NT) {
-    const int gj = g.gj0 + j0 - 2 + r;
-    const bool ok = gj >= 0 && gj < g.NJ;
-    X.cN[r] = ok ? __ldg(F.cN + gj) : 0.0;
-    X.cS[r] = ok ? __ldg(F.cS + gj) : 0.0;
-  }
-  if (hasf) {
-    for (int idx = threadIdx.x; idx < (SH - 2) * SW; idx += NT) {
-      const int r = 1 + idx / SW, c = idx - (r - 1) * SW;
-      const int jl = j0 - 2 + r, i = i0 - 2 + c;
-      uint8_t fv = 0;
-      if (i >= 0 && i < g.ni && jl >= -kGhost && jl < g.nj + kGhost) fv = F.flag[g.off(i, jl)];
-      X.f[r][c] = fv;
-    }
-  }
-  __syncthreads();
-  const double omega = A.omega, omc = A.omc, beta = A.beta;
-  // red sweep on the tile and its 1-node ring (rows j0-1 .. j0+TY)
-  for (int idx = threadIdx.x; idx < (SH - 2) * (SW / 2); idx += NT) {
-    const int r = 1 + idx / (SW / 2), cp = idx - (r - 1) * (SW / 2);
-    const int jl = j0 - 2 + r, gj = g.gj0 + jl;
-    const int c = 2 * cp + (gj & 1);
-    if (c < 1 || c > SW - 2 || jl < -1 || jl > g.nj) continue;
-    const int gi = i0 - 2 + c;
-    if (gi < F.ui0 || gi >= F.ui1 || gj < F.uj0 || gj >= F.uj1) continue;
-    const uint8_t fl = hasf ? X.f[r][c] : (uint8_t)0;
-    double aE, aW, aN, aS, aP;
-    if (HELM) {
-      if (fl != FLUID) continue;
-      const double cE = X.cE[c], cW = X.cW[c], cN = X.cN[r], cS = X.cS[r], cD = X.cD[c];
-      aE = beta * cE; aW = beta * cW; aN = beta * cN; aS = beta * cS;
-      aP = 1.0 + beta * (((cE + cW) + (cN + cS)) + cD);
-    } else {
-      if (fl & PF_INACTIVE) continue;
-      aE = (fl & PF_E) ? 0.0 : X.cE[c];
-      aW = (fl & PF_W) ? 0.0 : X.cW[c];
-      aN = (fl & PF_N) ? 0.0 : X.cN[r];
-      aS = (fl & PF_S) ? 0.0 : X.cS[r];
-      aP = ((aE + aW) + (aN + aS)) + X.cD[c];
-    }
-    const double xo = S.x[r][c];
-    const double s = (aE * S.x[r][c + 1] + aW * S.x[r][c - 1]) + (aN * S.x[r + 1][c] + aS * S.x[r - 1][c]);
-    const double gs = (S.b[r - 1][c] + s) / aP;
-    S.x[r][c] = omc * xo + omega * gs;
-    if (r >= 2 && r <= SH - 3 && c >= 2 && c <= SW - 3 && jl < g.nj)
-      tmax = umax64(tmax, (unsigned long long)__double_as_longlong(fabs(gs - xo)));
-  }
-  __syncthreads();
-  // black sweep on the tile (rows j0 .. j0+TY-1)
-  for (int idx = threadIdx.x; idx < (SH - 4) * (SW / 2); idx += NT) {
-    const int r = 2 + idx / (SW / 2), cp = idx - (r - 2) * (SW / 2);
-    const int jl = j0 - 2 + r, gj = g.gj0 + jl;
-    const int c = 2 * cp + 1 - (gj & 1);
-    if (c < 2 || c > SW - 3 || jl >= g.nj) continue;
-    const int gi = i0 - 2 + c;
-    if (gi < F.ui0 || gi >= F.ui1 || gj < F.uj0 || gj >= F.uj1) continue;
-    const uint8_t fl = hasf ? X.f[r][c] : (uint8_t)0;
-    double aE, aW, aN, aS, aP;
-    if (HELM) {
-      if (fl != FLUID) continue;
-      const double cE = X.cE[c], cW = X.cW[c], cN = X.cN[r], cS = X.cS[r], cD = X.cD[c];
-      aE = beta * cE; aW = beta * cW; aN = beta * cN; aS = beta * cS;
-      aP = 1.0 + beta * (((cE + cW) + (cN + cS)) + cD);
-    } else {
-      if (fl & PF_INACTIVE) continue;
-      aE = (fl & PF_E) ? 0.0 : X.cE[c];
-      aW = (fl & PF_W) ? 0.0 : X.cW[c];
-      aN = (fl & PF_N) ? 0.0 : X.cN[r];
-      aS = (fl & PF_S) ? 0.0 : X.cS[r];
-      aP = ((aE + aW) + (aN + aS)) + X.cD[c];
-    }
-    const double xo = S.x[r][c];
-    const double s = (aE * S.x[r][c + 1] + aW * S.x[r][c - 1]) + (aN * S.x[r + 1][c] + aS * S.x[r - 1][c]);
-    const double gs = (S.b[r - 1][c] + s) / aP;
-    S.x[r][c] = omc * xo + omega * gs;
-    tmax = umax64(tmax, (unsigned long long)__double_as_longlong(fabs(gs - xo)));
-  }
-  __syncthreads();
-  // store the owned tile (both colours, updated or not) to the output buffer
-  for (int idx = threadIdx.x; idx < TY * (TX / 2); idx += NT) {
-    const int rr = idx / (TX / 2), m = idx - rr * (TX / 2);
-    const int jl = j0 + rr, i = i0 + 2 * m;
-    if (jl >= g.nj || i >= g.ni) continue;
-    double *row = F.xout + (long)(jl + kGhost) * g.pitch;
-    const double a = S.x[rr + 2][2 * m + 2], b = S.x[rr + 2][2 * m + 3];
-    if (i + 1 < g.ni)
-      *reinterpret_cast<double2 *>(row + i) = make_double2(a, b);
-    else
-      row[i] = a;
-  }
-}
-
-__device__ __forceinline__ void sor_decide(SorCtl *ctl, unsigned long long rb, int k, int maxit, int ce, double tol) {
-  const double rho = __longlong_as_double((long long)rb);
-  const bool nan_ = isnan(rho);
-  const bool conv = (k % ce == 0) && rho <= tol;
-  if (nan_ || conv || k >= maxit) {
-    ctl->rho_final = rb;
-    ctl->status = nan_ ? 3 : (conv ? 0 : 1);
-    __threadfence();
-    ctl->k_done = k;
-  }
-}
-
-template <int HELM>
-__global__ void __launch_bounds__(NT, 2) k_sor(const __grid_constant__ SorArgs A) {
-  if (*(volatile int *)&A.ctl->k_done >= 0) return;  // converged at an earlier iteration
-  extern __shared__ unsigned char smraw[];
-  unsigned char *base = (unsigned char *)(((uintptr_t)smraw + 127) & ~(uintptr_t)127);
-  SorStage *stage = reinterpret_cast<SorStage *>(base);
-  SorAux &X = *reinterpret_cast<SorAux *>(base + 2 * sizeof(SorStage));
-  const int nt0 = A.f[0].tiles_x * A.f[0].tiles_y;
-  const int total = A.total_tiles;
-  if (threadIdx.x == 0) {
-    mbar_init(&X.bar[0], 1);
-    mbar_init(&X.bar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (threadIdx.x == 0 && (int)blockIdx.x < total) sor_issue(A, blockIdx.x, nt0, stage[0], &X.bar[0]);
-  unsigned long long tmax = 0;
-  int n = 0;
-  for (int t = blockIdx.x; t < total; t += gridDim.x, ++n) {
-    const int s = n & 1;
-    const int tn = t + gridDim.x;
-    if (threadIdx.x == 0 && tn < total) {
-      // stage s^1 was released by the __syncthreads that ended tile n-1
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      sor_issue(A, tn, nt0, stage[s ^ 1], &X.bar[s ^ 1]);
-    }
-    mbar_wait(&X.bar[s], (n >> 1) & 1);
-    int tt;
-    const SorFam &F = fam_of(A, t, nt0, tt);
-    sor_tile<HELM>(F, stage[s], X, tt, A, tmax);
-    __syncthreads();
-  }
-#pragma unroll
-  for (int off = 16; off; off >>= 1) tmax = umax64(tmax, __shfl_xor_sync(0xffffffffu, tmax, off));
-  if ((threadIdx.x & 31) == 0) X.wmax[threadIdx.x >> 5] = tmax;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long mx = 0;
-#pragma unroll
-    for (int w = 0; w < NT / 32; ++w) mx = umax64(mx, X.wmax[w]);
-    if (mx) atomicMax(&A.rho_bits[A.k], mx);
-    if (!A.multi) {
-      __threadfence();
-      const unsigned tk = atomicAdd(&A.ctl->ticket, 1u);
-      if (tk == gridDim.x - 1) {
-        const unsigned long long rb = atomicAdd(&A.rho_bits[A.k], 0ull);
-        A.ctl->ticket = 0;
-        sor_decide(A.ctl, rb, A.k, A.maxit, A.check_every, A.tol);
-      }
-    }
-  }
-}
-
-// multi-slab variant of the decision: runs after the rho all-reduce
-__global__ void k_sor_check(SorCtl *ctl, const unsigned long long *rho_bits, int k, int maxit, int ce, double tol) {
-  if (ctl->k_done >= 0) return;
-  sor_decide(ctl, rho_bits[k], k, maxit, ce, tol);
-}
-
 // ---------------------------------------------------------------- outlet fill (R10)
 __global__ void k_outlet_fill(double *__restrict__ us, Geo g, int nx) {
   int jl = blockIdx.x * blockDim.x + threadIdx.x;
@@ -745,38 +490,6 @@ int launch_predictor(const Ctx &c, const Slab &s, double yb, double vb) {
   k_pred_u<<<grid2(s.gu.ni, s.gu.nj, blk), blk, 0, c.stream>>>(A);
   k_pred_v<<<grid2(s.gv.ni, s.gv.nj, blk), blk, 0, c.stream>>>(A);
   return 2;
-}
-
-static int g_sor_blocks[2] = {0, 0};
-
-int sor_grid(const SorArgs &a) {
-  const int h = a.helmholtz ? 1 : 0;
-  if (!g_sor_blocks[h]) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (h) {
-      cudaFuncSetAttribute(k_sor<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSorSmem);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sor<1>, NT, kSorSmem);
-    } else {
-      cudaFuncSetAttribute(k_sor<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSorSmem);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sor<0>, NT, kSorSmem);
-    }
-    g_sor_blocks[h] = (per > 0 ? per : 1) * (sms > 0 ? sms : 1);
-  }
-  return a.total_tiles < g_sor_blocks[h] ? a.total_tiles : g_sor_blocks[h];
-}
-
-void launch_sor_iteration(const SorArgs &a, cudaStream_t s, int grid) {
-  if (a.helmholtz)
-    k_sor<1><<<grid, NT, kSorSmem, s>>>(a);
-  else
-    k_sor<0><<<grid, NT, kSorSmem, s>>>(a);
-}
-
-void launch_sor_check(SorCtl *ctl, const unsigned long long *rho_bits, int k, int maxit, int check_every,
-                      double tol, cudaStream_t s) {
-  k_sor_check<<<1, 1, 0, s>>>(ctl, rho_bits, k, maxit, check_every, tol);
 }
 
 int launch_outlet_fill(const Ctx &c, const Slab &s, double *us) {
