@@ -246,6 +246,40 @@ bool make_map(CUtensorMap *m, double *base, const Geo &g, int box_h) {
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 1-D coefficient array as a 2-D map of one row (rank-1 maps are rejected by
+// the driver on this image); OOB elements are zero-filled
+int g_last_encode = 0;
+bool make_map_1d(CUtensorMap *m, double *base, int n, int box_n) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)n, 1};
+  cuuint64_t strides[1] = {(cuuint64_t)((n * sizeof(double) + 15) / 16 * 16)};
+  cuuint32_t box[2] = {(cuuint32_t)box_n, 1};
+  cuuint32_t es[2] = {1, 1};
+  g_last_encode = (int)fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, dims, strides, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return g_last_encode == CUDA_SUCCESS;
+}
+
+bool make_coef_maps(Ctx &c) {
+  const Metric &m = c.m;
+  double *arr[3][5] = {{m.cEu, m.cWu, m.cDu, m.cNu, m.cSu},
+                       {m.cEv, m.cWv, m.cDv, m.cNv, m.cSv},
+                       {m.cEp, m.cWp, m.cDp, m.cNp, m.cSp}};
+  const int ncol[3] = {c.nx + 1, c.nx, c.nx}, nrow[3] = {c.ny, c.ny + 1, c.ny};
+  for (int f = 0; f < 3; ++f)
+    for (int k = 0; k < 5; ++k)
+      if (!make_map_1d(&c.tm_coef[f][k], arr[f][k], k < 3 ? ncol[f] : nrow[f], k < 3 ? kSorBoxW : kSorBoxHx)) {
+        c.err = "cuTensorMapEncodeTiled (coefficients f=" + std::to_string(f) + " k=" + std::to_string(k) +
+                " n=" + std::to_string(k < 3 ? ncol[f] : nrow[f]) + " ptr%256=" +
+                std::to_string((uintptr_t)arr[f][k] % 256) + " map%64=" + std::to_string((uintptr_t)&c.tm_coef[f][k] % 64) +
+                ") -> " + std::to_string(g_last_encode);
+        return false;
+      }
+  return true;
+}
+
 bool make_maps(Slab &s) {
   bool ok = true;
   for (int q = 0; q < 2; ++q) {
@@ -372,8 +406,9 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
     a.multi = mult ? 1 : 0;
     auto fam = [&](SorFam &f, const Geo &g, const double *b, const uint8_t *flag, const BBox &box,
                    const double *cE, const double *cW, const double *cD, const double *cN, const double *cS, int ui0,
-                   int ui1, int uj0, int uj1) {
+                   int ui1, int uj0, int uj1, int fid) {
       f.g = g; f.b = b; f.flag = flag; f.box = box;
+      for (int k = 0; k < 5; ++k) f.tmc[k] = c.tm_coef[fid][k];
       f.cE = cE; f.cW = cW; f.cD = cD; f.cN = cN; f.cS = cS;
       f.ui0 = ui0; f.ui1 = ui1; f.uj0 = uj0; f.uj1 = uj1;
       f.tiles_x = (g.ni + kSorTileX - 1) / kSorTileX;
@@ -381,12 +416,12 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
     };
     const Metric &m = c.m;
     if (helm) {
-      fam(a.f[0], s.gu, s.ru, s.tu, s.bu, m.cEu, m.cWu, m.cDu, m.cNu, m.cSu, 1, c.nx, 0, c.ny);
-      fam(a.f[1], s.gv, s.rv, s.tv, s.bv, m.cEv, m.cWv, m.cDv, m.cNv, m.cSv, 0, c.nx, 1, c.ny);
+      fam(a.f[0], s.gu, s.ru, s.tu, s.bu, m.cEu, m.cWu, m.cDu, m.cNu, m.cSu, 1, c.nx, 0, c.ny, 0);
+      fam(a.f[1], s.gv, s.rv, s.tv, s.bv, m.cEv, m.cWv, m.cDv, m.cNv, m.cSv, 0, c.nx, 1, c.ny, 1);
       a.nfam = 2;
     } else {
       BBox pb = s.bpb;
-      fam(a.f[0], s.gp, s.bp, s.pf, pb, m.cEp, m.cWp, m.cDp, m.cNp, m.cSp, 0, c.nx, 0, c.ny);
+      fam(a.f[0], s.gp, s.bp, s.pf, pb, m.cEp, m.cWp, m.cDp, m.cNp, m.cSp, 0, c.nx, 0, c.ny, 2);
       a.nfam = 1;
     }
     a.total_tiles = a.f[0].tiles_x * a.f[0].tiles_y + (a.nfam == 2 ? a.f[1].tiles_x * a.f[1].tiles_y : 0);
@@ -626,6 +661,7 @@ int ibm_init(const ibm_config *cfg, void *d_workspace, size_t bytes, void *cuda_
     return fail(IBM_ERR_ARG);
   }
   carve(c, (char *)d_workspace);
+  if (!make_coef_maps(c)) return fail(IBM_ERR_CUDA);
   for (Slab &s : c.sl)
     if (!make_maps(s)) {
       c.err = "cuTensorMapEncodeTiled unavailable or failed";

@@ -43,6 +43,7 @@ struct BBox {  // half-open node-index box: global columns, LOCAL rows
 struct SorFam {
   CUtensorMap tmx;      // TMA map of the input iterate (box SW x SH)
   CUtensorMap tmb;      // TMA map of the right-hand side (box SW x SH-2)
+  CUtensorMap tmc[5];   // 1-D maps of the coefficients: cE, cW, cD (box SW columns), cN, cS (box SH global rows)
   const double *xin;
   double *xout;
   const double *b;
@@ -106,6 +107,7 @@ struct Ctx {
   cudaStream_t stream;
   Metric m;
   std::vector<Slab> sl;
+  CUtensorMap tm_coef[3][5];  // [u, v, p][cE, cW, cD, cN, cS] (1-D TMA descriptors)
   unsigned long long *rho_bits;
   SorCtl *ctl;
   int *nanflag;
