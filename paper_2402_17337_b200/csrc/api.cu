@@ -62,6 +62,16 @@ int check_config(const ibm_config *cfg, std::string &why) {
     if (!(cfg->xn[i + 1] > cfg->xn[i])) { why = "xn not strictly increasing"; return IBM_ERR_CONFIG; }
   for (int j = 0; j < cfg->ny; ++j)
     if (!(cfg->yn[j + 1] > cfg->yn[j])) { why = "yn not strictly increasing"; return IBM_ERR_CONFIG; }
+  // spacings within [2^-300, 2^300]: every stencil coefficient and SOR diagonal then
+  // lies in [2^-700, 2^700], the range the SOR kernel's division fast path assumes
+  for (int i = 0; i < cfg->nx; ++i) {
+    const double h = cfg->xn[i + 1] - cfg->xn[i];
+    if (!(h >= 0x1p-300 && h <= 0x1p300)) { why = "xn spacing outside [2^-300, 2^300]"; return IBM_ERR_CONFIG; }
+  }
+  for (int j = 0; j < cfg->ny; ++j) {
+    const double h = cfg->yn[j + 1] - cfg->yn[j];
+    if (!(h >= 0x1p-300 && h <= 0x1p300)) { why = "yn spacing outside [2^-300, 2^300]"; return IBM_ERR_CONFIG; }
+  }
   if (!(cfg->Re > 0)) { why = "Re <= 0"; return IBM_ERR_CONFIG; }
   if (!(cfg->dt > 0)) { why = "dt <= 0"; return IBM_ERR_CONFIG; }
   if (!(cfg->omega_p >= 1.0 && cfg->omega_p < 2.0)) { why = "omega_p outside [1,2)"; return IBM_ERR_CONFIG; }
