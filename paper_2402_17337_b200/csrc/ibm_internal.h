@@ -133,8 +133,8 @@ int launch_pflags(const Ctx &c, const Slab &s);
 int launch_predictor(const Ctx &c, const Slab &s, double yb, double vb);
 int sor_grid(const SorArgs &a);
 // TMA box of the SOR tile (x) and of its right-hand side (b)
-constexpr int kSorBoxW = 128, kSorBoxHx = 20, kSorBoxHb = 18;
-constexpr int kSorTileX = 124, kSorTileY = 16;
+constexpr int kSorBoxW = 64, kSorBoxHx = 20, kSorBoxHb = 18;
+constexpr int kSorTileX = 60, kSorTileY = 16;
 void launch_sor_iteration(const SorArgs &a, cudaStream_t st, int grid);
 void launch_sor_check(SorCtl *ctl, const unsigned long long *rho_bits, int k, int maxit, int check_every,
                       double tol, cudaStream_t st);
