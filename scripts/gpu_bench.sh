@@ -1,17 +1,21 @@
 #!/bin/bash
-# One GPU session: tests, bench, ncu launch list and a full capture of the top kernels.
-# Usage (from the repo root, under gpurun): bash scripts/gpu_bench.sh [tag]
-set -x
+# One GPU session: smoke, bench (JSON line), ncu launch list of the bench command
+# and full captures of the Poisson SOR pass and the other kernels.
+# Usage (from the repo root, under gpurun): bash scripts/gpu_bench.sh TAG
 TAG=${1:-r01}
 mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > gpurun_out/gpu_${TAG}.txt 2>&1
-grep -E "MemTotal|MemAvailable" /proc/meminfo >> gpurun_out/gpu_${TAG}.txt; nproc >> gpurun_out/gpu_${TAG}.txt
-python __graft_entry__.py smoke > gpurun_out/smoke_${TAG}.log 2>&1
-python bench.py > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_${TAG}.csv \
-    python bench.py --steps 1 --warmup 0 --maxit-p 100 --maxit-uv 20 --no-e2e --no-cpu-baseline --no-clocks > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:'k_sor<0>' -s 10 -c 2 \
-    -o gpurun_out/prof_sor_${TAG} -f python bench.py --steps 1 --warmup 0 --maxit-p 30 --maxit-uv 10 --no-e2e --no-cpu-baseline --no-clocks > gpurun_out/ncu_sor_${TAG}.log 2>&1
-ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:'k_pred|k_prhs|k_correct|k_sor<1>' -c 8 \
-    -o gpurun_out/prof_other_${TAG} -f python bench.py --steps 1 --warmup 0 --maxit-p 5 --maxit-uv 3 --no-e2e --no-cpu-baseline --no-clocks > gpurun_out/ncu_other_${TAG}.log 2>&1
-ls -la gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total,power.limit --format=csv > gpurun_out/gpu_${TAG}.txt 2>&1
+nproc >> gpurun_out/gpu_${TAG}.txt
+python __graft_entry__.py smoke > gpurun_out/smoke_${TAG}.log 2>&1; tail -1 gpurun_out/smoke_${TAG}.log
+python bench.py > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err; cat gpurun_out/bench_${TAG}.json
+# launch list (cold-cache, serialised): the bench command with a short Poisson cap
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
+    python bench.py --steps 1 --warmup 0 --maxit-p 200 --no-e2e --no-cpu-baseline --no-clocks > /dev/null 2>&1
+# full capture: a Poisson pass ~190 iterations into the first step, and the other kernels
+ncu --set full --clock-control none --import-source on -k regex:k_sor -s 205 -c 1 -o gpurun_out/prof_sor_${TAG} -f \
+    python bench.py --steps 1 --warmup 0 --maxit-p 220 --no-e2e --no-cpu-baseline --no-clocks > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:'k_pred|k_prhs|k_correct|k_classify|k_pflags|k_forces' -c 12 \
+    -o gpurun_out/prof_other_${TAG} -f python bench.py --steps 1 --warmup 0 --maxit-p 5 --maxit-uv 3 --no-e2e --no-cpu-baseline --no-clocks > /dev/null 2>&1
+ncu --set full --clock-control none -k regex:k_sor -s 2 -c 1 -o gpurun_out/prof_uvsor_${TAG} -f \
+    python bench.py --steps 1 --warmup 0 --maxit-p 5 --maxit-uv 10 --no-e2e --no-cpu-baseline --no-clocks > /dev/null 2>&1
+ls gpurun_out | grep ${TAG}
