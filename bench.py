@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--cpu-sample-n", type=int, default=0, help="oracle sample grid (0 = auto)")
+    ap.add_argument("--sor-batch", type=int, default=0,
+                    help="> 0: host-launched SOR iterations in batches of this size instead of the graph WHILE loop")
     return ap.parse_args()
 
 
@@ -226,7 +228,8 @@ def main():
         nccl_id = obj[0]
 
     cfg = I.cfg4(n=args.n, maxit_p=args.maxit_p, maxit_uv=args.maxit_uv)
-    g = P.Solver(cfg.xn, cfg.yn, device=local, rank=rank, nranks=world, nccl_id=nccl_id, **cfg.solver_kwargs())
+    g = P.Solver(cfg.xn, cfg.yn, device=local, rank=rank, nranks=world, nccl_id=nccl_id, sor_batch=args.sor_batch,
+                 **cfg.solver_kwargs())
     g.set_body(*cfg.body_args())
     u0, v0, p0 = I.initial_fields(cfg.nx, cfg.ny)
     j0, j1 = g.rows
