@@ -216,25 +216,21 @@ def main():
     import torch.distributed as dist
 
     import paper_2402_17337_b200 as P
+    from paper_2402_17337_b200.dist import bootstrap_nccl_id, max_over_ranks, slab_of
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
     nccl_id = None
     if world > 1:
-        obj = [P.ibm_nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        dist.init_process_group("nccl", device_id=dev)
+        nccl_id = bootstrap_nccl_id(rank)
 
     cfg = I.cfg4(n=args.n, maxit_p=args.maxit_p, maxit_uv=args.maxit_uv)
     g = P.Solver(cfg.xn, cfg.yn, device=local, rank=rank, nranks=world, nccl_id=nccl_id, sor_batch=args.sor_batch,
                  **cfg.solver_kwargs())
     g.set_body(*cfg.body_args())
-    u0, v0, p0 = I.initial_fields(cfg.nx, cfg.ny)
     j0, j1 = g.rows
-    last = j1 == cfg.ny
-    g.set_fields(u0[j0:j1], v0[j0:j1 + (1 if last else 0)], p0[j0:j1])
+    g.set_fields(*slab_of(*I.initial_fields(cfg.nx, cfg.ny), cfg.ny, world, rank))
     stream = g.stream
 
     def barrier():
@@ -260,10 +256,7 @@ def main():
     launches = int(sum(raw[k].launches for k in range(args.steps)))
     psor_ms = float(sum(raw[k].ms[3] for k in range(args.steps)))
     uvsor_ms = float(sum(raw[k].ms[1] for k in range(args.steps)))
-    if world > 1:
-        t = torch.tensor([t_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_ms = float(t.item())
+    t_ms = max_over_ranks(t_ms, dev)
     updates = updates_for(stats, cfg.nx, cfg.ny)
     value = updates / (t_ms / 1e3)
 
@@ -311,11 +304,7 @@ def main():
             M.ibm_get_fields(g.ctx, mask, ptrs, M.IBM_HOST)
         f1.record(stream)
         barrier()
-        te = f0.elapsed_time(f1)
-        if world > 1:
-            t = torch.tensor([te], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            te = float(t.item())
+        te = max_over_ranks(f0.elapsed_time(f1), dev)
         nbytes = sum(host[n].numel() * 8 for n in host)
         e2e = {"value": updates_for(np.concatenate(estats), cfg.nx, cfg.ny) / (te / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": te / args.steps}

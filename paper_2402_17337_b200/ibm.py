@@ -237,10 +237,8 @@ class Solver:
     def _rows(self):
         if self.loopback or self.nranks == 1:
             return 0, self.ny
-        base, rem = divmod(self.ny, self.nranks)
-        r = self.rank
-        j0 = r * base + min(r, rem)
-        return j0, j0 + base + (1 if r < rem else 0)
+        from .dist import slab_rows
+        return slab_rows(self.ny, self.nranks, self.rank)
 
     def shape(self, name):
         j0, j1 = self.rows
