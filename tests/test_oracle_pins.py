@@ -456,3 +456,53 @@ def test_paper_constants_golden():
     assert abs(g["k"]["value"] - I.PAPER_K) < 1e-15
     b = I.Body()
     assert b.b / b.a == I.THICKNESS_RATIO
+
+
+def test_forcing_target_linear_exact_including_second_node(oracle_mod):
+    """R14 / R14b: for forcing nodes with a single fluid neighbour (vertical), a
+    field linear along the column that takes the body velocity at the boundary
+    intercept is reproduced exactly -- both when the target extrapolates through
+    the neighbour N and when it switches to N2 (d_N < d_F).  A wrong distance or
+    node in either branch breaks the exactness."""
+    cfg = I.cfg1()
+    o = oracle_mod.Oracle(cfg.xn, cfg.yn, **cfg.solver_kwargs())
+    o.set_body(*cfg.body_args())
+    t = 0.07
+    o.classify_at(t)
+    b = cfg.body
+    ybar, ydot = oracle_mod.plunge(t, b.hbar, b.k)
+    yb = b.y0 + ybar
+    xc, yc = 0.5 * (cfg.xn[1:] + cfg.xn[:-1]), 0.5 * (cfg.yn[1:] + cfg.yn[:-1])
+    seen = {True: 0, False: 0}
+    for fam, name, xs, ys, uB in ((0, "tu", cfg.xn, yc, 0.0), (1, "tv", xc, cfg.yn, ydot)):
+        tag = o.get(name)
+        nj, ni = tag.shape
+        X, Y = np.meshgrid(xs, ys)
+        for j, i in zip(*np.nonzero(tag == 2)):
+            nbs = [(di, dj) for di, dj in ((1, 0), (-1, 0), (0, 1), (0, -1))
+                   if 0 <= i + di < ni and 0 <= j + dj < nj and tag[j + dj, i + di] == 0]
+            if len(nbs) != 1 or nbs[0][1] == 0:
+                continue
+            dj = nbs[0][1]
+            z = (xs[i] - b.x0) / b.a
+            yB = yb + dj * b.b * math.sqrt(1.0 - z * z)
+            dF, dN = abs(yB - ys[j]), abs(ys[j + dj] - yB)
+            field = uB + 0.7 * (Y - yB)
+            got = o.forcing_target(fam, field, int(i), int(j))
+            assert abs(got - (uB + 0.7 * (ys[j] - yB))) < 1e-12
+            seen[bool(dN < dF)] += 1
+    assert seen[True] > 5 and seen[False] > 5
+
+
+def test_long_run_bounded(oracle_mod):
+    """R9b / R14b: with the open-face pressure gradient and the N2 switch the
+    cfg1 foil stays bounded over 60 steps with converged Poisson solves (the
+    SPEC-literal readings diverge within ~40 steps)."""
+    cfg = I.cfg1(perturb=0.0, steps=60, omega_p=1.9, maxit_p=100000)
+    o = oracle_mod.Oracle(cfg.xn, cfg.yn, **cfg.solver_kwargs())
+    o.set_body(*cfg.body_args())
+    o.set_fields(*I.initial_fields(cfg.nx, cfg.ny))
+    st, stats = o.step(cfg.steps)
+    assert st == 0
+    assert np.abs(o.get("u")).max() < 3.0 and np.abs(o.get("v")).max() < 3.0
+    assert np.all(np.isfinite(stats[:, 5:7]))
