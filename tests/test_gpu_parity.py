@@ -93,7 +93,7 @@ def test_cfg1_unperturbed(mods):
 
 @pytest.mark.parametrize("nx,ny", [(130, 98), (257, 131), (64, 36)])
 def test_ragged_tiles(mods, nx, ny):
-    """Grids that leave ragged tiles in x and y (tile = 128 x 16 nodes)."""
+    """Grids that leave ragged tiles in x and y (SOR tile = 60 x 16 owned nodes)."""
     cfg = I.cfg1(nx=nx, ny=ny, steps=3, maxit_p=600)
     o, g, ro, rg = run_pair(mods, cfg, cfg.steps)
     assert_parity(o, g, ro, rg)
@@ -249,3 +249,34 @@ def test_full_size_loopback_invariance(mods):
         torch.cuda.empty_cache()
     assert np.array_equal(res[0][0][:, 1:5], res[1][0][:, 1:5])
     assert torch.equal(res[0][1], res[1][1]) and torch.equal(res[0][2], res[1][2])
+
+
+def test_full_size_parity_vs_oracle(mods):
+    """BJ configs[3] at its full size (8192^2 foil on the paper domain) in the
+    bench's launch configuration, one step with the SOR solves capped (20
+    Poisson / 10 velocity iterations so the oracle finishes in about a minute):
+    every field is compared with the oracle element by element."""
+    O, P = mods
+    import torch
+    cfg = I.cfg4(n=8192, maxit_p=20, maxit_uv=10)
+    u0, v0, p0 = I.initial_fields(cfg.nx, cfg.ny)
+    g = P.Solver(cfg.xn, cfg.yn, **cfg.solver_kwargs())
+    g.set_body(*cfg.body_args())
+    g.set_fields(u0, v0, p0)
+    sg, stg = g.step(1)
+    gpu = {n: g.get(n) for n in ("u", "v", "p", "phi", "q", "fu", "fv")}
+    g.close()
+    del g
+    torch.cuda.empty_cache()
+    o = O.Oracle(cfg.xn, cfg.yn, **cfg.solver_kwargs())
+    o.set_body(*cfg.body_args())
+    o.set_fields(u0, v0, p0)
+    so, sto = o.step(1)
+    assert sg == so
+    assert np.array_equal(stg[:, 1:5], sto[:, 1:5])
+    for n, a in gpu.items():
+        b = o.get(n)
+        assert rel_l2(a, b) <= FIELD_TOL, n
+        assert np.array_equal(a, b), (n, np.abs(a - b).max())
+    for col in (5, 6):
+        assert abs(stg[0, col] - sto[0, col]) <= FORCE_TOL * max(abs(sto[0, col]), 1e-30)
