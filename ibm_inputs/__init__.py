@@ -126,11 +126,15 @@ def cfg1(perturb=0.01, nx=128, ny=96, steps=10, **kw) -> Config:
 
 
 def cfg2(nx=512, ny=384, steps=2000, **kw) -> Config:
-    """BJ configs[1]: stationary circular cylinder Re=100, 512x384, h=1/16."""
+    """BJ configs[1]: stationary circular cylinder Re=100, 512x384, h=1/16.
+    omega_p = 1.9: with the S:327 default 1.5 the Poisson solve cannot reach
+    tol 1e-8 within 10^4 iterations on this grid and the under-converged
+    projection diverges by t ~ 1.4 (measured)."""
     xn = uniform_axis(-8.0, 24.0, nx)
     yn = uniform_axis(-12.0, 12.0, ny)
     body = Body(a=0.5, b=0.5, hbar=0.0, k=1.0)
     kw.setdefault("tol_p", 1e-8)
+    kw.setdefault("omega_p", 1.9)
     return Config("cfg2-cylinder-%dx%d" % (nx, ny), xn, yn, Re=100.0, dt=0.02, body=body,
                   steps=steps, perturb=0.0, **kw)
 

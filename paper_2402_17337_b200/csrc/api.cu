@@ -395,7 +395,8 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
   const double tol = iters_override > 0 ? -1.0 : (helm ? cfg.tol_uv : cfg.tol_p);
   const double omega = helm ? cfg.omega_uv : cfg.omega_p;
   CK(cudaMemsetAsync(c.rho_bits, 0, sizeof(unsigned long long) * (size_t)(maxit + 2), c.stream));
-  c.h_ctl[1] = SorCtl{0ull, -1, 0, 0u, 0};
+  std::memset(&c.h_ctl[1], 0, sizeof(SorCtl));
+  c.h_ctl[1].k_done = -1;
   CK(cudaMemcpyAsync(c.ctl, &c.h_ctl[1], sizeof(SorCtl), cudaMemcpyHostToDevice, c.stream));
   const bool mult = multi(c);
   std::vector<SorArgs> args(c.sl.size());
@@ -436,6 +437,29 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
     }
     a.total_tiles = a.f[0].tiles_x * a.f[0].tiles_y + (a.nfam == 2 ? a.f[1].tiles_x * a.f[1].tiles_y : 0);
     grids[r] = sor_grid(a);
+  }
+  if (!mult && iters_override <= 0 && cfg.sor_batch <= 0 && sor_coop_fits(args[0])) {
+    // small grid: the whole loop in one persistent cooperative launch
+    Slab &s = c.sl[0];
+    SorArgs &a = args[0];
+    if (helm) {
+      a.f[0].xb[0] = s.us[0]; a.f[0].xb[1] = s.us[1]; a.f[0].tmxb[0] = s.tm_us[0]; a.f[0].tmxb[1] = s.tm_us[1];
+      a.f[0].tmb = s.tm_ru;
+      a.f[1].xb[0] = s.vs[0]; a.f[1].xb[1] = s.vs[1]; a.f[1].tmxb[0] = s.tm_vs[0]; a.f[1].tmxb[1] = s.tm_vs[1];
+      a.f[1].tmb = s.tm_rv;
+    } else {
+      a.f[0].xb[0] = s.phi[0]; a.f[0].xb[1] = s.phi[1]; a.f[0].tmxb[0] = s.tm_phi[0]; a.f[0].tmxb[1] = s.tm_phi[1];
+      a.f[0].tmb = s.tm_bp;
+    }
+    CK(launch_sor_coop(a, s0, c.stream));
+    ++c.launches;
+    CK(cudaMemcpyAsync(&c.h_ctl[0], c.ctl, sizeof(SorCtl), cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    *k_out = c.h_ctl[0].k_done;
+    unsigned long long rb = c.h_ctl[0].rho_final;
+    std::memcpy(rho_out, &rb, sizeof(double));
+    *status = c.h_ctl[0].status;
+    return IBM_OK;
   }
   int &hint = helm ? c.hint_uv : c.hint_p;
   int batch = cfg.sor_batch > 0 ? cfg.sor_batch : std::max(4, std::min(hint, maxit));

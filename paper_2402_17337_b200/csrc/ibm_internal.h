@@ -46,6 +46,8 @@ struct SorFam {
   CUtensorMap tmc[5];   // 1-D maps of the coefficients: cE, cW, cD (box SW columns), cN, cS (box SH global rows)
   const double *xin;
   double *xout;
+  double *xb[2];        // both ping-pong buffers (persistent cooperative solve)
+  CUtensorMap tmxb[2];  // their TMA maps
   const double *b;
   const uint8_t *flag;  // pflags (Poisson) or tags (Helmholtz)
   Geo g;
@@ -62,6 +64,7 @@ struct SorCtl {  // per-solve device control block
   int status;                    // 0 converged, 1 maxit, 3 NaN
   unsigned ticket;               // last-block counter
   int pad;
+  unsigned long long rho3[3];    // persistent (cooperative) solve: residual of iteration k in slot k % 3
 };
 
 struct SorArgs {
@@ -132,6 +135,10 @@ int launch_classify(const Ctx &c, const Slab &s, double yb);
 int launch_pflags(const Ctx &c, const Slab &s);
 int launch_predictor(const Ctx &c, const Slab &s, double yb, double vb);
 int sor_grid(const SorArgs &a);
+// persistent cooperative solve (small grids): whole SOR loop in one launch with a grid
+// barrier per iteration; returns false when the problem does not fit one co-resident grid
+bool sor_coop_fits(const SorArgs &a);
+cudaError_t launch_sor_coop(const SorArgs &a, int s0, cudaStream_t st);
 // TMA box of the SOR tile (x) and of its right-hand side (b)
 constexpr int kSorBoxW = 64, kSorBoxHx = 20, kSorBoxHb = 18;
 constexpr int kSorTileX = 60, kSorTileY = 16;

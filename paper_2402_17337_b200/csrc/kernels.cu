@@ -27,6 +27,18 @@ __device__ __forceinline__ double2 ld2(const double *__restrict__ p, const Geo &
   return r;
 }
 
+// a / b for b > 0, bit-identical to IEEE division: a zero dividend (the common
+// case in uniform-flow regions) would send div.rn.f64 down its slow path, so a
+// safe 1.0 is divided instead (hidden behind an opaque move, otherwise the
+// compiler folds the substitution away) and the exact +-0 = a is selected.
+__device__ __forceinline__ double pdiv(double a, double b) {
+  const bool zero = (a == 0.0);
+  double d = zero ? 1.0 : a;
+  asm("mov.b64 %0, %0;" : "+d"(d));
+  const double q = d / b;
+  return zero ? a : q;
+}
+
 // ---------------------------------------------------------------- a1: classification
 // Solid = inside the ellipse (boundary inclusive); Forcing = Solid
 // with at least one in-range 4-neighbour outside.  Recomputed analytically for the
@@ -195,20 +207,20 @@ __global__ void k_pred_u(PredArgs A) {
   if (gj == ny - 1) {
     tn = 0.0;
   } else {
-    double un = (dy[gj + 1] * uC + dy[gj] * uN) / (dy[gj] + dy[gj + 1]);
-    double vn = (dx[i] * ld(v, gv, i - 1, jl + 1) + dx[i - 1] * ld(v, gv, i, jl + 1)) / (dx[i - 1] + dx[i]);
+    double un = pdiv(dy[gj + 1] * uC + dy[gj] * uN, dy[gj] + dy[gj + 1]);
+    double vn = pdiv(dx[i] * ld(v, gv, i - 1, jl + 1) + dx[i - 1] * ld(v, gv, i, jl + 1), dx[i - 1] + dx[i]);
     tn = un * vn;
   }
   if (gj == 0) {
     ts = 0.0;
   } else {
-    double us_ = (dy[gj] * uS + dy[gj - 1] * uC) / (dy[gj - 1] + dy[gj]);
-    double vs_ = (dx[i] * ld(v, gv, i - 1, jl) + dx[i - 1] * ld(v, gv, i, jl)) / (dx[i - 1] + dx[i]);
+    double us_ = pdiv(dy[gj] * uS + dy[gj - 1] * uC, dy[gj - 1] + dy[gj]);
+    double vs_ = pdiv(dx[i] * ld(v, gv, i - 1, jl) + dx[i - 1] * ld(v, gv, i, jl), dx[i - 1] + dx[i]);
     ts = us_ * vs_;
   }
-  const double C = (ue * ue - uw * uw) / hxc[i] + (tn - ts) / dy[gj];
+  const double C = pdiv(ue * ue - uw * uw, hxc[i]) + pdiv(tn - ts, dy[gj]);
   const double Cp = A.have_hist ? A.cup[o] : C;
-  const double G = (ld(A.p, gp, i, jl) - ld(A.p, gp, i - 1, jl)) / hxc[i];
+  const double G = pdiv(ld(A.p, gp, i, jl) - ld(A.p, gp, i - 1, jl), hxc[i]);
   const double cE = A.m.cEu[i], cW = A.m.cWu[i], cD = A.m.cDu[i], cN = A.m.cNu[gj], cS = A.m.cSu[gj];
   const double L = ((cE * (uE - uC) + cW * (uW - uC)) + (cN * (uN - uC) + cS * (uS - uC))) - cD * uC;
   A.cu[o] = C;
@@ -222,7 +234,7 @@ __global__ void k_pred_u(PredArgs A) {
     double tgt = forcing_target(u, A.tu, g, A.bu, i, jl, A.m.xn, A.m.yc, A.B, 0.0);
     double uhat = uC + A.dt * ((-(1.5 * C - 0.5 * Cp) - G) + A.nu * L);
     A.us[o] = tgt;
-    A.fu[o] = (tgt - uhat) / A.dt;
+    A.fu[o] = pdiv(tgt - uhat, A.dt);
     A.ru[o] = 0.0;
   }
 }
@@ -257,19 +269,19 @@ __global__ void k_pred_v(PredArgs A) {
   const double vN = ld(v, g, i, jl + 1), vS = ld(v, g, i, jl - 1);
   double vn = 0.5 * (vC + vN);
   double vs_ = 0.5 * (vS + vC);
-  double ue = (dy[gj] * ld(u, gu, i + 1, jl - 1) + dy[gj - 1] * ld(u, gu, i + 1, jl)) / (dy[gj - 1] + dy[gj]);
-  double ve = (i == nx - 1) ? vC : (dx[i + 1] * vC + dx[i] * vE) / (dx[i] + dx[i + 1]);
+  double ue = pdiv(dy[gj] * ld(u, gu, i + 1, jl - 1) + dy[gj - 1] * ld(u, gu, i + 1, jl), dy[gj - 1] + dy[gj]);
+  double ve = (i == nx - 1) ? vC : pdiv(dx[i + 1] * vC + dx[i] * vE, dx[i] + dx[i + 1]);
   double te = ue * ve, tw;
   if (i == 0) {
     tw = 0.0;  // inlet corner: u = 1, v = 0
   } else {
-    double uw = (dy[gj] * ld(u, gu, i, jl - 1) + dy[gj - 1] * ld(u, gu, i, jl)) / (dy[gj - 1] + dy[gj]);
-    double vw = (dx[i] * vW + dx[i - 1] * vC) / (dx[i - 1] + dx[i]);
+    double uw = pdiv(dy[gj] * ld(u, gu, i, jl - 1) + dy[gj - 1] * ld(u, gu, i, jl), dy[gj - 1] + dy[gj]);
+    double vw = pdiv(dx[i] * vW + dx[i - 1] * vC, dx[i - 1] + dx[i]);
     tw = uw * vw;
   }
-  const double C = (te - tw) / dx[i] + (vn * vn - vs_ * vs_) / hyc[gj];
+  const double C = pdiv(te - tw, dx[i]) + pdiv(vn * vn - vs_ * vs_, hyc[gj]);
   const double Cp = A.have_hist ? A.cvp[o] : C;
-  const double G = (ld(A.p, gp, i, jl) - ld(A.p, gp, i, jl - 1)) / hyc[gj];
+  const double G = pdiv(ld(A.p, gp, i, jl) - ld(A.p, gp, i, jl - 1), hyc[gj]);
   const double cE = A.m.cEv[i], cW = A.m.cWv[i], cD = A.m.cDv[i], cN = A.m.cNv[gj], cS = A.m.cSv[gj];
   const double L = ((cE * (vE - vC) + cW * (vW - vC)) + (cN * (vN - vC) + cS * (vS - vC))) - cD * vC;
   A.cv[o] = C;
@@ -282,7 +294,7 @@ __global__ void k_pred_v(PredArgs A) {
     double tgt = forcing_target(v, A.tv, g, A.bv, i, jl, A.m.xc, A.m.yn, A.B, A.B.vb);
     double vhat = vC + A.dt * ((-(1.5 * C - 0.5 * Cp) - G) + A.nu * L);
     A.vs[o] = tgt;
-    A.fv[o] = (tgt - vhat) / A.dt;
+    A.fv[o] = pdiv(tgt - vhat, A.dt);
     A.rv[o] = 0.0;
   }
 }
@@ -319,8 +331,8 @@ __global__ void k_prhs(const double *__restrict__ us, const double *__restrict__
   const double mN = (gj + 1 == ny) ? 1.0 : ((f & PF_N) ? 0.0 : 1.0);
   const double mS = (gj == 0) ? 1.0 : ((f & PF_S) ? 0.0 : 1.0);
   const double dxi = m.dx[i], dyj = m.dy[gj];
-  const double rhs = (((mE * uE - mW * uW) / dxi) + ((mN * vN - mS * vS) / dyj)) / dt;
-  q[o] = (((1.0 - mE) * uE - (1.0 - mW) * uW) / dxi) + (((1.0 - mN) * vN - (1.0 - mS) * vS) / dyj);
+  const double rhs = pdiv(pdiv(mE * uE - mW * uW, dxi) + pdiv(mN * vN - mS * vS, dyj), dt);
+  q[o] = pdiv((1.0 - mE) * uE - (1.0 - mW) * uW, dxi) + pdiv((1.0 - mN) * vN - (1.0 - mS) * vS, dyj);
   bp[o] = -rhs;
 }
 
@@ -338,10 +350,10 @@ __global__ void k_correct_u(double *__restrict__ u, const double *__restrict__ u
   double val = us[o];
   if (i >= 1 && i <= nx - 1) {
     const uint8_t f = pbox.contains(i, jl) ? pf[gp.off(i, jl)] : (uint8_t)0;
-    if (!(f & PF_W)) val = us[o] - dt * ((phi[gp.off(i, jl)] - phi[gp.off(i - 1, jl)]) / m.hxc[i]);
+    if (!(f & PF_W)) val = us[o] - dt * pdiv(phi[gp.off(i, jl)] - phi[gp.off(i - 1, jl)], m.hxc[i]);
   } else if (i == nx) {
     const uint8_t f = pbox.contains(nx - 1, jl) ? pf[gp.off(nx - 1, jl)] : (uint8_t)0;
-    if (!(f & PF_INACTIVE)) val = us[o] - dt * ((0.0 - phi[gp.off(nx - 1, jl)]) / (0.5 * m.dx[nx - 1]));
+    if (!(f & PF_INACTIVE)) val = us[o] - dt * pdiv(0.0 - phi[gp.off(nx - 1, jl)], 0.5 * m.dx[nx - 1]);
   }
   u[o] = val;
   if (!isfinite(val)) atomicOr(nanflag, 1);
@@ -358,7 +370,7 @@ __global__ void k_correct_v(double *__restrict__ v, const double *__restrict__ v
   double val = vs[o];
   if (gj >= 1 && gj <= ny - 1) {
     const uint8_t f = pbox.contains(i, jl) ? pf[gp.off(i, jl)] : (uint8_t)0;
-    if (!(f & PF_S)) val = vs[o] - dt * ((phi[gp.off(i, jl)] - phi[gp.off(i, jl - 1)]) / m.hyc[gj]);
+    if (!(f & PF_S)) val = vs[o] - dt * pdiv(phi[gp.off(i, jl)] - phi[gp.off(i, jl - 1)], m.hyc[gj]);
   }
   v[o] = val;
   if (!isfinite(val)) atomicOr(nanflag, 1);

@@ -280,3 +280,24 @@ def test_full_size_parity_vs_oracle(mods):
         assert np.array_equal(a, b), (n, np.abs(a - b).max())
     for col in (5, 6):
         assert abs(stg[0, col] - sto[0, col]) <= FORCE_TOL * max(abs(sto[0, col]), 1e-30)
+
+
+def test_persistent_and_launched_sor_agree(mods):
+    """The persistent cooperative SOR loop (small grids) and the per-iteration
+    launches (host-batched) give bit-identical results on a grid that fits the
+    co-resident grid."""
+    O, P = mods
+    cfg = I.cfg1(nx=1024, ny=768, steps=2, maxit_p=300, maxit_uv=50)
+    u0, v0, p0 = I.initial_fields(cfg.nx, cfg.ny, cfg.perturb)
+    out = []
+    for kw in ({}, {"sor_batch": 64}):
+        g = P.Solver(cfg.xn, cfg.yn, **cfg.solver_kwargs(), **kw)
+        g.set_body(*cfg.body_args())
+        g.set_fields(u0, v0, p0)
+        st, stats = g.step(cfg.steps)
+        out.append((st, stats, {n: g.get(n) for n in ("u", "v", "p", "phi")}))
+        g.close()
+    assert out[0][0] == out[1][0]
+    assert np.array_equal(out[0][1][:, 1:5], out[1][1][:, 1:5])
+    for n in ("u", "v", "p", "phi"):
+        assert np.array_equal(out[0][2][n], out[1][2][n]), n
