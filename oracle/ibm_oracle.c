@@ -639,8 +639,13 @@ static int step_once(orc_ctx *c)
         if (st == ORC_ERR_DIVERGED) return ORC_ERR_DIVERGED;
         if (st == ORC_WARN_NOCONV) status = ORC_WARN_NOCONV;
     }
-    /* outlet fill u*_{nx} = u*_{nx-1} (R10) */
-    for (int j = 0; j < ny; ++j) c->us[UI(c, nx, j)] = c->us[UI(c, nx - 1, j)];
+    /* outlet fill (R10b): u*_{nx} from discrete continuity of the last cell column,
+     * u*_{nx} = u*_{nx-1} - dx_{nx-1} (v*_N - v*_S)/dy.  The SPEC-literal
+     * zero-gradient fill injects divergence wherever dv/dy != 0 at the
+     * outlet and makes the time integration non-convergent. */
+    for (int j = 0; j < ny; ++j)
+        c->us[UI(c, nx, j)] = c->us[UI(c, nx - 1, j)] -
+                              c->dx[nx - 1] * ((c->vs[VI(c, nx - 1, j + 1)] - c->vs[VI(c, nx - 1, j)]) / c->dy[j]);
 
     /* a5: mass source q and Poisson rhs on the masks built above (R16) */
     for (int j = 0; j < ny; ++j)

@@ -557,11 +557,10 @@ int step_once(Ctx &c, ibm_step_stats *st) {
   if (sst == 3) { c.err = "velocity SOR residual is NaN at step " + std::to_string(c.step + 1); return IBM_ERR_DIVERGED; }
   if (sst == 1) status = IBM_WARN_NOCONV;
   const int ures = ku & 1;
-  for (Slab &s : c.sl) c.launches += launch_outlet_fill(c, s, s.us[ures]);
-  if (multi(c)) {
-    HALO((*b = s.us[ures], *g = &s.gu));
-    HALO((*b = s.vs[ures], *g = &s.gv));
-  }
+  // the outlet fill (R10b) reads v* one row up: exchange v* first, then u*
+  if (multi(c)) HALO((*b = s.vs[ures], *g = &s.gv));
+  for (Slab &s : c.sl) c.launches += launch_outlet_fill(c, s, s.us[ures], s.vs[ures]);
+  if (multi(c)) HALO((*b = s.us[ures], *g = &s.gu));
   CK(cudaEventRecord(c.ev[2], c.stream));
   // a5 masks -> q, Poisson rhs; phi := 0 on inactive cells
   for (Slab &s : c.sl) c.launches += launch_prhs(c, s, s.us[ures], s.vs[ures], s.phi[c.phi_cur]);

@@ -145,7 +145,7 @@ constexpr int kSorTileX = 60, kSorTileY = 16;
 void launch_sor_iteration(const SorArgs &a, cudaStream_t st, int grid);
 void launch_sor_check(SorCtl *ctl, const unsigned long long *rho_bits, int k, int maxit, int check_every,
                       double tol, cudaStream_t st);
-int launch_outlet_fill(const Ctx &c, const Slab &s, double *us);
+int launch_outlet_fill(const Ctx &c, const Slab &s, double *us, const double *vs);
 int launch_prhs(const Ctx &c, const Slab &s, const double *us, const double *vs, double *phi_start);
 int launch_correct(const Ctx &c, const Slab &s, const double *us, const double *vs, const double *phi);
 int launch_forces(const Ctx &c, const Slab &s);

@@ -299,11 +299,16 @@ __global__ void k_pred_v(PredArgs A) {
   }
 }
 
-// ---------------------------------------------------------------- outlet fill (R10)
-__global__ void k_outlet_fill(double *__restrict__ us, Geo g, int nx) {
+// ---------------------------------------------------------------- outlet fill (R10b)
+// u*_{nx} = u*_{nx-1} - dx_{nx-1} (v*_N - v*_S)/dy: discrete continuity of the last
+// cell column (the v* halo row is exchanged before this kernel on slabs).
+__global__ void k_outlet_fill(double *__restrict__ us, const double *__restrict__ vs, Geo gu, Geo gv, Metric m,
+                              int nx) {
   int jl = blockIdx.x * blockDim.x + threadIdx.x;
-  if (jl >= g.nj) return;
-  us[g.off(nx, jl)] = us[g.off(nx - 1, jl)];
+  if (jl >= gu.nj) return;
+  const int gj = gu.gj0 + jl;
+  us[gu.off(nx, jl)] = us[gu.off(nx - 1, jl)] -
+                       m.dx[nx - 1] * pdiv(vs[gv.off(nx - 1, jl + 1)] - vs[gv.off(nx - 1, jl)], m.dy[gj]);
 }
 
 // ---------------------------------------------------------------- a5: Poisson rhs and q
@@ -504,8 +509,8 @@ int launch_predictor(const Ctx &c, const Slab &s, double yb, double vb) {
   return 2;
 }
 
-int launch_outlet_fill(const Ctx &c, const Slab &s, double *us) {
-  k_outlet_fill<<<(s.gu.nj + 127) / 128, 128, 0, c.stream>>>(us, s.gu, c.nx);
+int launch_outlet_fill(const Ctx &c, const Slab &s, double *us, const double *vs) {
+  k_outlet_fill<<<(s.gu.nj + 127) / 128, 128, 0, c.stream>>>(us, vs, s.gu, s.gv, c.m, c.nx);
   return 1;
 }
 

@@ -506,3 +506,32 @@ def test_long_run_bounded(oracle_mod):
     assert st == 0
     assert np.abs(o.get("u")).max() < 3.0 and np.abs(o.get("v")).max() < 3.0
     assert np.all(np.isfinite(stats[:, 5:7]))
+
+
+def test_temporal_order_second(oracle_mod):
+    """P:54 (R7): AB2 convection + CN diffusion + incremental projection are second
+    order in time.  Self-convergence on a fixed 48x32 grid from a discretely
+    divergence-free start (streamfunction on cell corners, vanishing at the inlet
+    and walls): successive differences at T fall 4x per dt halving (3.2-4.8).
+    This also pins the outlet reading R10b -- the SPEC-literal zero-gradient
+    fill makes these differences stagnate."""
+    nx, ny, L, H = 48, 32, 3.0, 2.0
+    xn, yn = I.uniform_axis(0.0, L, nx), I.uniform_axis(-1.0, 1.0, ny)
+    Xc, Yc = np.meshgrid(xn, yn)
+    psi = Yc + 0.05 * np.sin(math.pi * Xc / L) ** 2 * np.sin(math.pi * (Yc + 1) / H) ** 2
+    u0 = (psi[1:, :] - psi[:-1, :]) / np.diff(yn)[:, None]
+    v0 = -(psi[:, 1:] - psi[:, :-1]) / np.diff(xn)[None, :]
+    u0[:, 0], v0[0, :], v0[-1, :] = 1.0, 0.0, 0.0
+    T, res = 0.02, []
+    for dt in (0.01, 0.005, 0.0025, 0.00125):
+        o = oracle_mod.Oracle(xn, yn, Re=50.0, dt=dt, omega_p=1.8, tol_p=1e-13, maxit_p=200000, omega_uv=1.2,
+                              tol_uv=1e-14, maxit_uv=10000)
+        o.clear_body()
+        o.set_fields(u0, v0, np.zeros((ny, nx)))
+        st, _ = o.step(int(round(T / dt)))
+        assert st == 0
+        res.append((o.get("u"), o.get("v")))
+    for k in (0, 1):
+        e = [np.abs(res[i][k] - res[i + 1][k]).max() for i in range(3)]
+        for i in range(2):
+            assert 3.2 <= e[i] / e[i + 1] <= 4.8, (k, e)
