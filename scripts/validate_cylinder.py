@@ -37,6 +37,24 @@ def strouhal(t, cl, D=1.0, U=1.0, window=0.5):
     return D / (U * period), ups
 
 
+def surface_pressure_force(p, tp, xn, yn):
+    """Diagnostic: pressure force on the body from the active cells bordering the
+    inactive (body) cells, p x face length summed over those faces; (c_d, c_l)."""
+    act = tp == 0
+    dx, dy = np.diff(xn), np.diff(yn)
+    fx = fy = 0.0
+    # x-faces: active cell west of a body cell pushes +x; east of it pushes -x
+    w = act[:, :-1] & ~act[:, 1:]
+    e = ~act[:, :-1] & act[:, 1:]
+    fx += (p[:, :-1][w] * np.broadcast_to(dy[:, None], w.shape)[w]).sum()
+    fx -= (p[:, 1:][e] * np.broadcast_to(dy[:, None], e.shape)[e]).sum()
+    s_ = act[:-1, :] & ~act[1:, :]
+    n_ = ~act[:-1, :] & act[1:, :]
+    fy += (p[:-1, :][s_] * np.broadcast_to(dx[None, :], s_.shape)[s_]).sum()
+    fy -= (p[1:, :][n_] * np.broadcast_to(dx[None, :], n_.shape)[n_]).sum()
+    return 2.0 * fx, 2.0 * fy
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=2000)
@@ -67,7 +85,9 @@ def main():
     t, cd, cl = S[:, 0], S[:, 5], S[:, 6]
     St, ups = strouhal(t, cl)
     n0 = len(t) // 2
+    cdp, clp = surface_pressure_force(g.get("p"), g.get("tp"), cfg.xn, cfg.yn)
     res = {"config": cfg.describe(), "steps_done": len(t), "status": int(status), "wall_s": wall,
+           "cd_last": float(cd[-1]), "cd_surface_pressure_last": float(cdp), "cl_surface_pressure_last": float(clp),
            "St": St, "n_crossings": len(ups), "mean_cd_last_half": float(np.mean(cd[n0:])),
            "cl_amplitude_last_half": float(0.5 * (cl[n0:].max() - cl[n0:].min())),
            "it_p_mean": float(S[:, 2].mean()), "it_p_max": float(S[:, 2].max()), "it_uv_mean": float(S[:, 1].mean()),
