@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--cpu-sample-n", type=int, default=0, help="oracle sample grid (0 = auto)")
+    ap.add_argument("--sor-fuse", type=int, default=0,
+                    help="Poisson iterations fused per HBM pass (0 = library default 2; slabs use 1)")
     ap.add_argument("--sor-batch", type=int, default=0,
                     help="> 0: host-launched SOR iterations in batches of this size instead of the graph WHILE loop")
     return ap.parse_args()
@@ -228,7 +230,7 @@ def main():
 
     cfg = I.cfg4(n=args.n, maxit_p=args.maxit_p, maxit_uv=args.maxit_uv)
     g = P.Solver(cfg.xn, cfg.yn, device=local, rank=rank, nranks=world, nccl_id=nccl_id, sor_batch=args.sor_batch,
-                 **cfg.solver_kwargs())
+                 sor_fuse=args.sor_fuse, **cfg.solver_kwargs())
     g.set_body(*cfg.body_args())
     j0, j1 = g.rows
     g.set_fields(*slab_of(*I.initial_fields(cfg.nx, cfg.ny), cfg.ny, world, rank))
@@ -261,12 +263,17 @@ def main():
     updates = updates_for(stats, cfg.nx, cfg.ny)
     value = updates / (t_ms / 1e3)
 
-    # roofline of the dominant kernel (Poisson red-black SOR pass): algorithmic
-    # bytes per launch = 24 B x this rank's p cells; duration from CUDA events
-    # bracketing the Poisson loop on the launch stream, / iterations
+    # roofline of the dominant kernel (the Poisson pass: k_sor_wf fusing m
+    # red-black iterations per HBM pass, or k_sor with m = 1 on slabs):
+    # algorithmic bytes per launch = 24 B x this rank's p cells (phi in, b in,
+    # phi out once per pass); launch duration = CUDA events bracketing the
+    # Poisson loop on the launch stream / passes (it_p / m per step)
     Np_local = cfg.nx * (j1 - j0)
     it_p = float(stats[:, 2].sum())
-    avg_launch_s = (psor_ms / 1e3) / max(it_p, 1.0)
+    fuse = 1 if world > 1 else (args.sor_fuse or 2)
+    passes = float(sum(np.ceil(stats[:, 2] / fuse)))
+    avg_iter_s = (psor_ms / 1e3) / max(it_p, 1.0)
+    avg_launch_s = (psor_ms / 1e3) / max(passes, 1.0)
     achieved = BYTES_PER_POISSON_UPDATE * Np_local / avg_launch_s / 1e9
     peaks = {}
     try:
@@ -277,7 +284,7 @@ def main():
     traffic = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
-        traffic = prof.get("k_sor_poisson", {}).get("dram_bytes_per_cell", None)
+        traffic = prof.get("k_sor_wf_poisson" if fuse > 1 else "k_sor_poisson", {}).get("dram_bytes_per_cell", None)
         if traffic is not None:
             traffic = float(traffic) * Np_local
     except Exception:
@@ -326,10 +333,12 @@ def main():
                        "l2": "inputs larger than L2 (%.1f GB workspace, 126 MB L2)" % (g.ws.numel() / 1e9),
                        "parallelism": "slab%d" % world},
             "it_p": stats[:, 2].tolist(), "it_uv": stats[:, 1].tolist(),
-            "poisson_ms_per_iteration": 1e3 * avg_launch_s, "uv_sor_ms": uvsor_ms / args.steps,
+            "poisson_ms_per_iteration": 1e3 * avg_iter_s, "poisson_ms_per_pass": 1e3 * avg_launch_s,
+            "sor_fuse": fuse, "uv_sor_ms": uvsor_ms / args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_sor<0> (fused red-black Poisson pass)",
+                         "kernel": ("k_sor_wf<%d> (%d red-black Poisson iterations per HBM pass)" % (fuse, fuse)
+                                    if fuse > 1 else "k_sor<0> (one red-black Poisson iteration per HBM pass)"),
                          "bytes_per_launch": BYTES_PER_POISSON_UPDATE * Np_local, "peak_source": peak_src},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
         }

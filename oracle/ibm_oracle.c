@@ -296,8 +296,9 @@ typedef struct {
 /* Runs red-black SOR on nsys independent systems jointly: one iteration = red
  * sweep of every system, then black sweep of every system; rho_k = max over all
  * updates of |gs - x_old|.  Node update (R2, R13):
- *   s = fma(aE, xE, aW*xW) + fma(aN, xN, aS*xS);  gs = (b + s)/aP;
- *   x = fma(1-omega, x_old, omega*gs).  Colour red = (i+j) even.  Returns iterations; status
+ *   s = fma(aE, xE, aW*xW) + fma(aN, xN, aS*xS);  gs = (b + s) * (1/aP);
+ *   x = fma(1-omega, x_old, omega*gs).  1/aP is the correctly rounded reciprocal
+ *   (one IEEE division), then one IEEE multiplication -- reading R13.  Colour red = (i+j) even.  Returns iterations; status
  * ORC_ERR_DIVERGED if rho is NaN, ORC_WARN_NOCONV if maxit reached above tol. */
 static int sor_run(int nsys, sor_sys *sys, double omega, double tol, int maxit,
                    int check_every, double *rho_out, int *status)
@@ -322,7 +323,8 @@ static int sor_run(int nsys, sor_sys *sys, double omega, double tol, int maxit,
                         double xS = fv_at(S->x, S->ni, S->nj, i, j - 1);
                         /* R13: two explicit fused multiply-adds (C99 fma, one rounding each) */
                         double sum = fma(S->aE[id], xE, S->aW[id] * xW) + fma(S->aN[id], xN, S->aS[id] * xS);
-                        double gs = (S->b[id] + sum) / S->aP[id];
+                        double rcp = 1.0 / S->aP[id];
+                        double gs = (S->b[id] + sum) * rcp;
                         double xo = S->x[id];
                         double e = fabs(gs - xo);
                         S->x[id] = fma(omc, xo, omega * gs);

@@ -13,8 +13,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libibm_b200.so")
-SOURCES = ["kernels.cu", "sor.cu", "api.cu"]
-HEADERS = ["ibm_internal.h", os.path.join("..", "..", "include", "ibm.h")]
+SOURCES = ["kernels.cu", "sor.cu", "sor_wf.cu", "api.cu"]
+HEADERS = ["ibm_internal.h", "sor_common.cuh", os.path.join("..", "..", "include", "ibm.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -36,10 +36,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
+    extra = os.environ.get("IBM_NVCC_DEFS", "").split()  # tuning experiments only (-DNAME=value)
     objs = []
     for src in SOURCES:
         obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        cmd = [nvcc, *NVCC_FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [nvcc, *NVCC_FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
         out = subprocess.run(cmd, capture_output=True, text=True)
         if out.returncode != 0:
             sys.stderr.write(out.stdout + out.stderr)

@@ -84,6 +84,7 @@ int check_config(const ibm_config *cfg, std::string &why) {
   }
   if (cfg->ny / cfg->nranks < 4) { why = "slabs need >= 4 rows"; return IBM_ERR_CONFIG; }
   if (cfg->nranks > 1 && !cfg->loopback && !cfg->nccl_id) { why = "nccl_id required for nranks > 1"; return IBM_ERR_CONFIG; }
+  if (cfg->sor_fuse < 0 || cfg->sor_fuse > kWfMaxM) { why = "sor_fuse outside [0, 4]"; return IBM_ERR_CONFIG; }
   return IBM_OK;
 }
 
@@ -290,8 +291,13 @@ bool make_coef_maps(Ctx &c) {
   return true;
 }
 
-bool make_maps(Slab &s) {
+bool make_maps(Slab &s, int wf_m) {
   bool ok = true;
+  if (wf_m >= 2) {
+    ok = ok && make_map(&s.tm_wphi[0], s.phi[0], s.gp, wf_box_rows(wf_m));
+    ok = ok && make_map(&s.tm_wphi[1], s.phi[1], s.gp, wf_box_rows(wf_m));
+    ok = ok && make_map(&s.tm_wbp, s.bp, s.gp, wf_box_rows(wf_m));
+  }
   for (int q = 0; q < 2; ++q) {
     ok = ok && make_map(&s.tm_phi[q], s.phi[q], s.gp, kSorBoxHx);
     ok = ok && make_map(&s.tm_us[q], s.us[q], s.gu, kSorBoxHx);
@@ -389,7 +395,14 @@ int refresh_time(Ctx &c) {
 // ---------------------------------------------------------------- SOR driver
 // Launches iterations in batches; each iteration kernel early-exits once the
 // device control block says converged, so the host polls once per batch.
-int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *status, int iters_override) {
+// One SOR solve from the iterate in buffer s0.  Passes are launched in
+// batches between convergence polls; a pass is one iteration (k_sor) or, for the
+// single-slab Poisson system, wf_m fused iterations (k_sor_wf).  The pass's last
+// CTA takes the convergence decision on the device; if it stops at an iteration
+// inside a fused pass, that pass is replayed from its (intact) input buffer up to
+// the decided iteration.  *buf_out receives the buffer index of the result.
+int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *status, int iters_override,
+              int *buf_out) {
   const ibm_config &cfg = c.cfg;
   const int maxit = iters_override > 0 ? iters_override : (helm ? cfg.maxit_uv : cfg.maxit_p);
   const double tol = iters_override > 0 ? -1.0 : (helm ? cfg.tol_uv : cfg.tol_p);
@@ -459,54 +472,112 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
     unsigned long long rb = c.h_ctl[0].rho_final;
     std::memcpy(rho_out, &rb, sizeof(double));
     *status = c.h_ctl[0].status;
+    *buf_out = (s0 + *k_out) & 1;
     return IBM_OK;
   }
+  // temporally blocked Poisson passes (single slab)
+  const bool wf = !helm && !mult && c.wf_m >= 2;
+  WfArgs wa;
+  if (wf) {
+    std::memset(&wa, 0, sizeof(wa));
+    const Slab &s = c.sl[0];
+    const SorFam &f = args[0].f[0];
+    wa.tmb = s.tm_wbp;
+    wa.flag = f.flag; wa.g = f.g; wa.box = f.box;
+    wa.cE = f.cE; wa.cW = f.cW; wa.cD = f.cD; wa.cN = f.cN; wa.cS = f.cS;
+    wa.ui0 = f.ui0; wa.ui1 = f.ui1; wa.uj0 = f.uj0; wa.uj1 = f.uj1;
+    wa.omega = omega; wa.omc = 1.0 - omega; wa.tol = tol;
+    wa.maxit = maxit; wa.check_every = cfg.check_every;
+    wa.rho_bits = c.rho_bits; wa.ctl = c.ctl;
+    wf_plan(wa, c.wf_m);
+  }
+  // one single-iteration pass of every slab (halos first when decomposed)
+  auto single = [&](int kk, int in, bool fixup) -> int {
+    const int out = in ^ 1;
+    if (mult) {
+      if (helm) {
+        HALO((*b = s.us[in], *g = &s.gu));
+        HALO((*b = s.vs[in], *g = &s.gv));
+      } else {
+        HALO((*b = s.phi[in], *g = &s.gp));
+      }
+    }
+    for (size_t r = 0; r < c.sl.size(); ++r) {
+      Slab &s = c.sl[r];
+      SorArgs &a = args[r];
+      a.k = kk;
+      a.fixup = fixup ? 1 : 0;
+      if (helm) {
+        a.f[0].xin = s.us[in]; a.f[0].xout = s.us[out]; a.f[0].tmx = s.tm_us[in]; a.f[0].tmb = s.tm_ru;
+        a.f[1].xin = s.vs[in]; a.f[1].xout = s.vs[out]; a.f[1].tmx = s.tm_vs[in]; a.f[1].tmb = s.tm_rv;
+      } else {
+        a.f[0].xin = s.phi[in]; a.f[0].xout = s.phi[out]; a.f[0].tmx = s.tm_phi[in]; a.f[0].tmb = s.tm_bp;
+      }
+      launch_sor_iteration(a, c.stream, grids[r]);
+      ++c.launches;
+    }
+    if (mult && !fixup) {
+      if (!c.loopback)
+        NK(ncclAllReduce(c.rho_bits + kk, c.rho_bits + kk, 1, ncclUint64, ncclMax, (ncclComm_t)c.nccl, c.stream));
+      launch_sor_check(c.ctl, c.rho_bits, kk, maxit, cfg.check_every, tol, c.stream);
+      ++c.launches;
+    }
+    return IBM_OK;
+  };
+  struct Pass {
+    int k0, m, in;
+  };
+  std::vector<Pass> passes;
   int &hint = helm ? c.hint_uv : c.hint_p;
   int batch = cfg.sor_batch > 0 ? cfg.sor_batch : std::max(4, std::min(hint, maxit));
-  int k = 1;
+  int k = 1, cur = s0;
   for (;;) {
     const int kend = std::min(maxit, k + batch - 1);
-    for (int kk = k; kk <= kend; ++kk) {
-      const int in = (s0 + kk - 1) & 1, out = (s0 + kk) & 1;
-      if (mult) {
-        if (helm) {
-          HALO((*b = s.us[in], *g = &s.gu));
-          HALO((*b = s.vs[in], *g = &s.gv));
-        } else {
-          HALO((*b = s.phi[in], *g = &s.gp));
-        }
-      }
-      for (size_t r = 0; r < c.sl.size(); ++r) {
-        Slab &s = c.sl[r];
-        SorArgs &a = args[r];
-        a.k = kk;
-        if (helm) {
-          a.f[0].xin = s.us[in]; a.f[0].xout = s.us[out]; a.f[0].tmx = s.tm_us[in]; a.f[0].tmb = s.tm_ru;
-          a.f[1].xin = s.vs[in]; a.f[1].xout = s.vs[out]; a.f[1].tmx = s.tm_vs[in]; a.f[1].tmb = s.tm_rv;
-        } else {
-          a.f[0].xin = s.phi[in]; a.f[0].xout = s.phi[out]; a.f[0].tmx = s.tm_phi[in]; a.f[0].tmb = s.tm_bp;
-        }
-        launch_sor_iteration(a, c.stream, grids[r]);
+    while (k <= kend) {
+      if (wf && k + c.wf_m - 1 <= maxit) {
+        wa.k = k;
+        wa.xout = c.sl[0].phi[cur ^ 1];
+        wa.tmx = c.sl[0].tm_wphi[cur];
+        CK(launch_sor_wf(wa, c.wf_m, c.stream));
         ++c.launches;
+        passes.push_back({k, c.wf_m, cur});
+        k += c.wf_m;
+      } else {
+        int r = single(k, cur, false);
+        if (r) return r;
+        passes.push_back({k, 1, cur});
+        k += 1;
       }
-      if (mult) {
-        if (!c.loopback)
-          NK(ncclAllReduce(c.rho_bits + kk, c.rho_bits + kk, 1, ncclUint64, ncclMax, (ncclComm_t)c.nccl, c.stream));
-        launch_sor_check(c.ctl, c.rho_bits, kk, maxit, cfg.check_every, tol, c.stream);
-        ++c.launches;
-      }
+      cur ^= 1;
     }
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(&c.h_ctl[0], c.ctl, sizeof(SorCtl), cudaMemcpyDeviceToHost, c.stream));
     CK(cudaStreamSynchronize(c.stream));
     if (c.h_ctl[0].k_done >= 0) break;
-    k = kend + 1;
     if (cfg.sor_batch <= 0) batch = std::min(2 * batch, 1024);
   }
-  *k_out = c.h_ctl[0].k_done;
+  const int kd = c.h_ctl[0].k_done;
+  *k_out = kd;
   unsigned long long rb = c.h_ctl[0].rho_final;
   std::memcpy(rho_out, &rb, sizeof(double));
   *status = c.h_ctl[0].status;
+  // the pass that holds iteration kd; replay a fused pass that overshot it
+  int buf = -1;
+  for (const Pass &p : passes)
+    if (kd >= p.k0 && kd < p.k0 + p.m) {
+      buf = p.in ^ 1;
+      if (kd < p.k0 + p.m - 1) {
+        int in = p.in;
+        for (int kk = p.k0; kk <= kd; ++kk, in ^= 1) {
+          int r = single(kk, in, true);
+          if (r) return r;
+        }
+        buf = in;
+      }
+      break;
+    }
+  if (buf < 0) { c.err = "SOR stopped at an iteration no pass covers"; return IBM_ERR_STATE; }
+  *buf_out = buf;
   if (iters_override <= 0) hint = *k_out;
   return IBM_OK;
 }
@@ -551,12 +622,12 @@ int step_once(Ctx &c, ibm_step_stats *st) {
   // a4 velocity (Helmholtz) SOR, u and v jointly (R5)
   int ku = 0, sst = 0;
   double rho_uv = 0.0;
-  int r = sor_solve(c, true, 0, &ku, &rho_uv, &sst, 0);
+  int ures = 0;
+  int r = sor_solve(c, true, 0, &ku, &rho_uv, &sst, 0, &ures);
   if (r) return r;
   if (st) { st->it_uv = ku; st->rho_uv = rho_uv; }
   if (sst == 3) { c.err = "velocity SOR residual is NaN at step " + std::to_string(c.step + 1); return IBM_ERR_DIVERGED; }
   if (sst == 1) status = IBM_WARN_NOCONV;
-  const int ures = ku & 1;
   // the outlet fill (R10b) reads v* one row up: exchange v* first, then u*
   if (multi(c)) HALO((*b = s.vs[ures], *g = &s.gv));
   for (Slab &s : c.sl) c.launches += launch_outlet_fill(c, s, s.us[ures], s.vs[ures]);
@@ -569,12 +640,13 @@ int step_once(Ctx &c, ibm_step_stats *st) {
   // a6 Poisson SOR, warm start
   int kp = 0;
   double rho_p = 0.0;
-  r = sor_solve(c, false, c.phi_cur, &kp, &rho_p, &sst, 0);
+  int pbuf = c.phi_cur;
+  r = sor_solve(c, false, c.phi_cur, &kp, &rho_p, &sst, 0, &pbuf);
   if (r) return r;
   if (st) { st->it_p = kp; st->rho_p = rho_p; }
   if (sst == 3) { c.err = "pressure SOR residual is NaN at step " + std::to_string(c.step + 1); return IBM_ERR_DIVERGED; }
   if (sst == 1) status = IBM_WARN_NOCONV;
-  c.phi_cur = (c.phi_cur + kp) & 1;
+  c.phi_cur = pbuf;
   if (multi(c)) HALO((*b = s.phi[c.phi_cur], *g = &s.gp));
   CK(cudaEventRecord(c.ev[4], c.stream));
   // a7 projection
@@ -678,6 +750,8 @@ int ibm_init(const ibm_config *cfg, void *d_workspace, size_t bytes, void *cuda_
   c.nccl = nullptr;
   c.hint_uv = 16;
   c.hint_p = 64;
+  // temporal blocking of the Poisson pass needs 2 m halo rows: single slab only
+  c.wf_m = (cfg->loopback || cfg->nranks > 1) ? 1 : (cfg->sor_fuse == 0 ? 2 : cfg->sor_fuse);
   if (c.loopback)
     for (int r = 0; r < cfg->nranks; ++r) c.sl.push_back(make_slab(*cfg, r));
   else
@@ -696,7 +770,7 @@ int ibm_init(const ibm_config *cfg, void *d_workspace, size_t bytes, void *cuda_
   carve(c, (char *)d_workspace);
   if (!make_coef_maps(c)) return fail(IBM_ERR_CUDA);
   for (Slab &s : c.sl)
-    if (!make_maps(s)) {
+    if (!make_maps(s, c.wf_m)) {
       c.err = "cuTensorMapEncodeTiled unavailable or failed";
       return fail(IBM_ERR_CUDA);
     }
@@ -916,9 +990,10 @@ int ibm_poisson_iterate(ibm_ctx *ctx, int iters, double *rho_out) {
   CK(cudaSetDevice(c.device));
   int k = 0, sst = 0;
   double rho = 0.0;
-  int r = sor_solve(c, false, c.phi_cur, &k, &rho, &sst, iters);
+  int pbuf = c.phi_cur;
+  int r = sor_solve(c, false, c.phi_cur, &k, &rho, &sst, iters, &pbuf);
   if (r) return r;
-  c.phi_cur = (c.phi_cur + k) & 1;
+  c.phi_cur = pbuf;
   if (rho_out) *rho_out = rho;
   return sst == 3 ? IBM_ERR_DIVERGED : IBM_OK;
 }

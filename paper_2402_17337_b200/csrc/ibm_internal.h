@@ -77,7 +77,28 @@ struct SorArgs {
   unsigned long long *rho_bits;  // [maxit + 2], zeroed per solve
   SorCtl *ctl;
   int multi;  // 1: several slabs / ranks -> decision in k_sor_check after the reduction
+  int fixup;  // 1: replay of iterations already decided (no early exit, no residual, no decision)
 };
+
+// Temporally blocked Poisson pass (sor_wf.cu): WM red-black iterations per HBM
+// pass.  One warp = one work item = a strip of 64 stored columns (64 - 4 WM
+// owned) x a segment of L owned rows, streamed top to bottom.
+struct WfArgs {
+  CUtensorMap tmx;      // iterate, box 64 x (2 WM + 2) rows
+  CUtensorMap tmb;      // right-hand side, same box
+  double *xout;
+  const uint8_t *flag;  // Poisson cell flags
+  Geo g;
+  BBox box;             // body envelope (local rows)
+  const double *cE, *cW, *cD, *cN, *cS;
+  int ui0, ui1, uj0, uj1;
+  int strips, segs, L, items;
+  double omega, omc, tol;
+  int k, maxit, check_every;
+  unsigned long long *rho_bits;
+  SorCtl *ctl;
+};
+constexpr int kWfMaxM = 4;  // fused iterations per pass: 2..kWfMaxM instantiated
 
 struct Metric {  // device pointers, global index space
   double *xn, *yn, *dx, *dy, *xc, *yc, *hxc, *hyc;
@@ -101,6 +122,7 @@ struct Slab {
   double *red;       // force partial sums [4]
   // TMA descriptors of the SOR operands (built once at init)
   CUtensorMap tm_phi[2], tm_bp, tm_us[2], tm_ru, tm_vs[2], tm_rv;
+  CUtensorMap tm_wphi[2], tm_wbp;  // boxes of the temporally blocked Poisson pass (rows 2 wf_m + 2)
 };
 
 struct Ctx {
@@ -124,6 +146,7 @@ struct Ctx {
   double Mx, My;
   double last_t, last_cd, last_cl;
   int hint_uv, hint_p;
+  int wf_m;         // Poisson iterations fused per HBM pass (1 = unfused k_sor)
   int launches;     // kernels launched in the current step
   cudaEvent_t ev[8];
   void *nccl;      // ncclComm_t when nranks > 1 and !loopback
@@ -143,6 +166,10 @@ cudaError_t launch_sor_coop(const SorArgs &a, int s0, cudaStream_t st);
 constexpr int kSorBoxW = 64, kSorBoxHx = 20, kSorBoxHb = 18;
 constexpr int kSorTileX = 60, kSorTileY = 16;
 void launch_sor_iteration(const SorArgs &a, cudaStream_t st, int grid);
+// temporally blocked Poisson pass: rows of the TMA box, segment length, launch
+int wf_box_rows(int m);
+void wf_plan(WfArgs &a, int m);
+cudaError_t launch_sor_wf(const WfArgs &a, int m, cudaStream_t st);
 void launch_sor_check(SorCtl *ctl, const unsigned long long *rho_bits, int k, int maxit, int check_every,
                       double tol, cudaStream_t st);
 int launch_outlet_fill(const Ctx &c, const Slab &s, double *us, const double *vs);

@@ -1,0 +1,390 @@
+// Temporally blocked Poisson red-black SOR (kernel a6-wf): WM full
+// red-black iterations (R1-R3) per HBM pass.
+//
+// Why: the one-iteration pass (sor.cu) is HBM-bound at 24 B per cell per
+// iteration (x in, b in, x out).  Streaming WM iterations through registers
+// moves the same 24 B per cell once per WM iterations.
+//
+// Decomposition: one warp = one work item = a strip of 64 stored columns
+// (global i0 .. i0+63 with i0 = sx*OW - 2WM; the middle OW = 64 - 4WM columns
+// are owned) x a segment of L owned rows [j0, j1).  The warp streams its strip
+// in increasing j: row r enters a register window of W = 2WM+2 rows (lane l
+// holds columns 2l, 2l+1), then half-sweep h = 0 .. 2WM-1 (red, black, red, ...)
+// is applied to row r-1-h.  That is the oracle's sweep order restricted to the
+// strip: half-sweep h at row r-1-h reads rows r-2-h .. r-h, which half-sweep
+// h-1 has already finished (row r-h earlier in this step) and half-sweep h+1 has
+// not yet touched (it reaches row r-2-h later in this step).  Every half-sweep
+// invalidates one more column at each strip edge and one more row at each
+// segment end (their outside neighbours are not updated here); those cells are
+// recomputed by the neighbouring items and are never stored nor counted, so
+// every stored value and every residual term is bit-identical to the oracle's.
+//
+// Rows arrive by TMA in chunks of W rows (x and b, 64 x W boxes; the TMA unit
+// zero-fills outside the array, the oracle's "0 outside the family") into a
+// per-warp double-buffered stage armed on an mbarrier.  Chunks whose rows are
+// all inside the family, away from the body box and carry the segment's
+// reference row coefficients take a check-free path with per-column
+// reciprocals; the rest (domain edges, body, stretched rows) the predicated one.
+//
+// Arithmetic: identical to sor.cu (R13).
+#include <cstdlib>
+#include <type_traits>
+#include <utility>
+
+#include "ibm_internal.h"
+#include "sor_common.cuh"
+
+namespace ibm {
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int WNW = 4;  // warps per CTA (independent work items)
+constexpr int WNT = 32 * WNW;
+constexpr int WNSTG = 2;  // stages per warp
+
+template <int WM>
+struct __align__(128) WfStage {
+  double x[2 * WM + 2][64];
+  double b[2 * WM + 2][64];
+};
+template <int WM>
+constexpr size_t wf_smem() {
+  return (size_t)WNW * WNSTG * sizeof(WfStage<WM>) + (size_t)WNW * WNSTG * sizeof(unsigned long long);
+}
+#ifndef WF_MINB
+#define WF_MINB 3
+#endif
+// resident CTAs per SM the register budget is sized for (shared memory permitting)
+template <int WM>
+constexpr int wf_min_blocks() {
+  return (int)((220u * 1024u) / wf_smem<WM>()) < WF_MINB ? (int)((220u * 1024u) / wf_smem<WM>()) : WF_MINB;
+}
+
+// Per-lane column data of the two columns gi = i0 + 2l + e.
+struct WfCols {
+  double aE[2], aW[2], sEW[2], cD[2], aPu[2], yu[2];
+  bool in[2];  // column inside the family's updatable range
+};
+
+// One node update of the check-free path: element E of window slot Q.  EDGE:
+// the strip reaches past the family's columns; lanes outside keep their value.
+template <int W, int Q, int E, bool EDGE>
+__device__ __forceinline__ void wf_fast(double2 (&X)[W], const double2 (&B)[W], const WfCols &C, double aN,
+                                        double aS, double omega, double omc, bool own, unsigned long long &tmax) {
+  constexpr int QN = (Q + 1) % W, QS = (Q + W - 1) % W;
+  const int l = threadIdx.x & 31;
+  double xE, xW;
+  if (E == 0) {
+    xW = __shfl_sync(FULL, X[Q].y, (l + 31) & 31);
+    xE = X[Q].y;
+  } else {
+    xW = X[Q].x;
+    xE = __shfl_sync(FULL, X[Q].x, (l + 1) & 31);
+  }
+  const double xo = rd(X[Q], E), xN = rd(X[QN], E), xS = rd(X[QS], E);
+  const double sm = __fma_rn(C.aE[E], xE, C.aW[E] * xW) + __fma_rn(aN, xN, aS * xS);
+  const double gs = (rd(B[Q], E) + sm) * C.yu[E];
+  const double xn = __fma_rn(omc, xo, omega * gs);
+  wr(X[Q], E, (!EDGE || C.in[E]) ? xn : xo);
+  const unsigned long long e = (unsigned long long)__double_as_longlong(fabs(gs - xo));
+  tmax = (own && e > tmax) ? e : tmax;
+}
+
+// One node update of the predicated path (domain edges, body flags, arbitrary
+// row coefficients): the same per-cell logic as sor.cu's boundary tiles.
+template <int W, int Q, int E>
+__device__ __forceinline__ void wf_slow(double2 (&X)[W], const double2 (&B)[W], const WfCols &C, const WfArgs &A,
+                                        int r, int gi, bool hasf, double omega, double omc, bool own,
+                                        unsigned long long &tmax) {
+  constexpr int QN = (Q + 1) % W, QS = (Q + W - 1) % W;
+  const int l = threadIdx.x & 31;
+  const int gj = A.g.gj0 + r;
+  double cN = 0.0, cS = 0.0;  // 0 outside the family (oracle: out-of-range coefficient)
+  if (gj >= 0 && gj < A.g.NJ) {
+    cN = A.cN[gj];
+    cS = A.cS[gj];
+  }
+  bool u = gi >= A.ui0 && gi < A.ui1 && gj >= A.uj0 && gj < A.uj1;
+  uint8_t fl = 0;
+  if (hasf && u) fl = A.flag[A.g.off(gi, r)];
+  u = u && !(fl & PF_INACTIVE);
+  double aE = C.aE[E], aW = C.aW[E], aN = cN, aS = cS, aP;
+  if (fl) {
+    aE = (fl & PF_E) ? 0.0 : aE;
+    aW = (fl & PF_W) ? 0.0 : aW;
+    aN = (fl & PF_N) ? 0.0 : aN;
+    aS = (fl & PF_S) ? 0.0 : aS;
+    aP = ((aE + aW) + (aN + aS)) + C.cD[E];
+  } else {
+    aP = (C.sEW[E] + (cN + cS)) + C.cD[E];
+  }
+  double xE, xW;
+  if (E == 0) {
+    xW = __shfl_sync(FULL, X[Q].y, (l + 31) & 31);
+    xE = X[Q].y;
+  } else {
+    xW = X[Q].x;
+    xE = __shfl_sync(FULL, X[Q].x, (l + 1) & 31);
+  }
+  const double xo = rd(X[Q], E), xN = rd(X[QN], E), xS = rd(X[QS], E);
+  const double sm = __fma_rn(aE, xE, aW * xW) + __fma_rn(aN, xN, aS * xS);
+  const double gs = (rd(B[Q], E) + sm) * __drcp_rn(aP);
+  if (u) {
+    wr(X[Q], E, __fma_rn(omc, xo, omega * gs));
+    if (own) tmax = umax64(tmax, (unsigned long long)__double_as_longlong(fabs(gs - xo)));
+  }
+}
+
+// predicated global stores (no branch: the warp stays provably converged, so
+// the shuffles of the next step need no divergence check and ptxas can
+// interleave consecutive steps)
+__device__ __forceinline__ void st_pred(bool p, double *a, double2 v) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %0, 0;\n @q st.global.v2.f64 [%1], {%2, %3};\n}\n" ::"r"((int)p),
+               "l"(a), "d"(v.x), "d"(v.y)
+               : "memory");
+}
+__device__ __forceinline__ void st_pred1(bool p, double *a, double v) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %0, 0;\n @q st.global.f64 [%1], %2;\n}\n" ::"r"((int)p), "l"(a),
+               "d"(v)
+               : "memory");
+}
+
+// compile-time loop: f(std::integral_constant<int, i>) for i = 0 .. N-1
+template <class F, int... I>
+__device__ __forceinline__ void sfor_impl(F &&f, std::integer_sequence<int, I...>) {
+  (f(std::integral_constant<int, I>{}), ...);
+}
+template <int N, class F>
+__device__ __forceinline__ void sfor(F &&f) {
+  sfor_impl(f, std::make_integer_sequence<int, N>{});
+}
+
+// The W steps of one chunk (window slot q = row rb + q).  MODE 2: check-free
+// interior strip; 1: check-free edge strip; 0: predicated.  OWN: every row the
+// chunk touches is owned by the item (residual and stores need only the lane
+// test).  rb is even and W is even, so the slot and the colour element of every
+// half-sweep are compile-time constants.
+template <int WM, int TP, int MODE, bool OWN>
+__device__ __forceinline__ void wf_chunk(double2 (&X)[2 * WM + 2], double2 (&B)[2 * WM + 2],
+                                         const WfStage<WM> &S, const WfCols &C, const WfArgs &A, int rb, int j0,
+                                         int j1, int i0, bool lane_own, bool hasf, double cN0, double cS0,
+                                         unsigned long long (&tmax)[WM]) {
+  constexpr int W = 2 * WM + 2;
+  const int l = threadIdx.x & 31;
+  const double omega = A.omega, omc = A.omc;
+  const long pitch = A.g.pitch;
+  // stored row rb + q - 2WM of this lane's pair
+  double *const ob = A.xout + (long)(rb - 2 * WM + kGhost) * pitch + (i0 + 2 * l);
+  const bool pair_in = MODE == 2 || i0 + 2 * l + 1 < A.g.ni;
+  sfor<W>([&](auto qc) {
+    constexpr int q = decltype(qc)::value;
+    X[q] = *reinterpret_cast<const double2 *>(&S.x[q][2 * l]);
+    B[q] = *reinterpret_cast<const double2 *>(&S.b[q][2 * l]);
+    sfor<2 * WM>([&](auto hc) {
+      constexpr int h = decltype(hc)::value;
+      constexpr int Q = ((q - 1 - h) % W + W) % W;  // slot of row rb + q - 1 - h
+      constexpr int E = (TP + Q + h) & 1;           // red (h even): (i + j) even
+      const int r = rb + q - 1 - h;
+      const bool own = OWN ? lane_own : (lane_own && r >= j0 && r < j1);
+      if constexpr (MODE > 0)
+        wf_fast<W, Q, E, MODE == 1>(X, B, C, cN0, cS0, omega, omc, own, tmax[h / 2]);
+      else
+        wf_slow<W, Q, E>(X, B, C, A, r, i0 + 2 * l + E, hasf, omega, omc, own, tmax[h / 2]);
+    });
+    // row rb + q - 2WM has received its last half-sweep: store the owned columns
+    const int ro = rb + q - 2 * WM;
+    const double2 v = X[((q - 2 * WM) % W + W) % W];
+    const bool st = OWN ? lane_own : (lane_own && ro >= j0 && ro < j1);
+    st_pred(st && pair_in, ob + q * pitch, v);
+    if (MODE < 2) st_pred1(st && !pair_in, ob + q * pitch, v.x);
+  });
+}
+
+template <int WM, int TP>
+__global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __grid_constant__ WfArgs A) {
+  constexpr int W = 2 * WM + 2, OW = 64 - 4 * WM;
+  constexpr unsigned kBytes = 2u * W * 64 * 8;
+  if (*(volatile int *)&A.ctl->k_done >= 0) return;  // converged at an earlier iteration
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  __shared__ unsigned long long wmax[WNW][WM];
+  const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
+  WfStage<WM> *st = reinterpret_cast<WfStage<WM> *>(smraw) + w * WNSTG;
+  unsigned long long *bar =
+      reinterpret_cast<unsigned long long *>(smraw + (size_t)WNW * WNSTG * sizeof(WfStage<WM>)) + w * WNSTG;
+  unsigned long long tmax[WM];
+#pragma unroll
+  for (int i = 0; i < WM; ++i) tmax[i] = 0ull;
+  const int item = blockIdx.x * WNW + w;
+  if (item < A.items) {
+    const Geo &g = A.g;
+    const int sx = item % A.strips, sy = item / A.strips;
+    const int i0 = sx * OW - 2 * WM;  // global column of stored column 0
+    const int j0 = sy * A.L;          // owned local rows [j0, j1)
+    const int j1 = min(j0 + A.L, g.nj);
+    const int rs = j0 - 2 * WM;       // first streamed row
+    const int nch = ((j1 - j0) + 4 * WM + W - 1) / W;
+    if (l == 0) {
+      for (int s = 0; s < WNSTG; ++s) mbar_init(&bar[s], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      for (int c = 0; c < WNSTG && c < nch; ++c) {
+        mbar_expect_tx(&bar[c], kBytes);
+        tma_load_2d(&st[c].x[0][0], &A.tmx, i0, rs + c * W + kGhost, &bar[c]);
+        tma_load_2d(&st[c].b[0][0], &A.tmb, i0, rs + c * W + kGhost, &bar[c]);
+      }
+    }
+    __syncwarp();
+    const bool lane_own = l >= WM && l <= 31 - WM && i0 + 2 * l < g.ni;
+    const bool interior = i0 >= A.ui0 && i0 + 64 <= A.ui1;
+    const bool boxstrip = !A.box.empty() && i0 < A.box.i1 && i0 + 64 > A.box.i0;
+    // column coefficients (0 outside the family) and the reference row of the segment
+    const int jr = min(max(g.gj0 + j0 + A.L / 2, 1), g.NJ - 2);
+    const double cN0 = A.cN[jr], cS0 = A.cS[jr];
+    WfCols C;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int gi = i0 + 2 * l + e;
+      const bool in = gi >= 0 && gi < g.ni;
+      const double cE = in ? A.cE[gi] : 0.0, cW = in ? A.cW[gi] : 0.0;
+      C.cD[e] = in ? A.cD[gi] : 0.0;
+      C.aE[e] = cE;
+      C.aW[e] = cW;
+      C.sEW[e] = cE + cW;
+      C.aPu[e] = (C.sEW[e] + (cN0 + cS0)) + C.cD[e];
+      C.yu[e] = __drcp_rn(C.aPu[e]);
+      C.in[e] = gi >= A.ui0 && gi < A.ui1;
+    }
+    double2 X[W], B[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) X[q] = B[q] = make_double2(0.0, 0.0);
+    // row test of chunk c (rows rb-2WM .. rb+W-2), prefetched one chunk ahead
+    auto row_ok = [&](int c, double &pn, double &ps) -> bool {
+      const int r = rs + c * W - 2 * WM + l, gj = g.gj0 + r;
+      const bool in = l <= 4 * WM && gj >= A.uj0 && gj < A.uj1;
+      pn = in ? A.cN[gj] : 0.0;
+      ps = in ? A.cS[gj] : 0.0;
+      return in && !(boxstrip && r >= A.box.j0 && r < A.box.j1);
+    };
+    double pn, ps;
+    bool pin = row_ok(0, pn, ps);
+    for (int c = 0; c < nch; ++c) {
+      const int s = c % WNSTG;
+      const int rb = rs + c * W;
+      const bool good = l > 4 * WM || (pin && pn == cN0 && ps == cS0);
+      const bool fast = __all_sync(FULL, good);
+      const bool hasf = boxstrip && rb + W - 2 >= A.box.j0 && rb - 2 * WM < A.box.j1;
+      if (c + 1 < nch) pin = row_ok(c + 1, pn, ps);
+      mbar_wait_warp(&bar[s], (c / WNSTG) & 1);
+      const bool ownall = rb - 2 * WM >= j0 && rb + W - 2 < j1;
+      if (fast && interior && ownall)
+        wf_chunk<WM, TP, 2, true>(X, B, st[s], C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax);
+      else if (fast && interior)
+        wf_chunk<WM, TP, 2, false>(X, B, st[s], C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax);
+      else if (fast)
+        wf_chunk<WM, TP, 1, false>(X, B, st[s], C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax);
+      else
+        wf_chunk<WM, TP, 0, false>(X, B, st[s], C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax);
+      __syncwarp();
+      if (l == 0 && c + WNSTG < nch) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&bar[s], kBytes);
+        tma_load_2d(&st[s].x[0][0], &A.tmx, i0, rs + (c + WNSTG) * W + kGhost, &bar[s]);
+        tma_load_2d(&st[s].b[0][0], &A.tmb, i0, rs + (c + WNSTG) * W + kGhost, &bar[s]);
+      }
+    }
+  }
+  // residual of each fused iteration: warp -> CTA -> atomicMax on its bit pattern
+#pragma unroll
+  for (int i = 0; i < WM; ++i) {
+#pragma unroll
+    for (int off = 16; off; off >>= 1) tmax[i] = umax64(tmax[i], __shfl_xor_sync(FULL, tmax[i], off));
+    if (l == 0) wmax[w][i] = tmax[i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < WM; ++i) {
+      unsigned long long mx = 0;
+#pragma unroll
+      for (int v = 0; v < WNW; ++v) mx = umax64(mx, wmax[v][i]);
+      if (mx) atomicMax(&A.rho_bits[A.k + i], mx);
+    }
+    __threadfence();
+    const unsigned tk = atomicAdd(&A.ctl->ticket, 1u);
+    if (tk == gridDim.x - 1) {
+      A.ctl->ticket = 0;
+      // first of the WM iterations that stops the solve (same test as sor_decide)
+      for (int i = 0; i < WM; ++i) {
+        const int k = A.k + i;
+        const unsigned long long rb = atomicAdd(&A.rho_bits[k], 0ull);
+        const double rho = __longlong_as_double((long long)rb);
+        const bool nan_ = isnan(rho);
+        const bool conv = (k % A.check_every == 0) && rho <= A.tol;
+        if (nan_ || conv || k >= A.maxit) {
+          A.ctl->rho_final = rb;
+          A.ctl->status = nan_ ? 3 : (conv ? 0 : 1);
+          __threadfence();
+          A.ctl->k_done = k;
+          break;
+        }
+      }
+    }
+  }
+}
+
+template <int WM, int TP>
+int wf_blocks_per_sm() {
+  static int per = 0;
+  if (!per) {
+    cudaFuncSetAttribute(k_sor_wf<WM, TP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wf_smem<WM>());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sor_wf<WM, TP>, WNT, wf_smem<WM>());
+    if (per < 1) per = 1;
+  }
+  return per;
+}
+
+template <int WM>
+cudaError_t wf_launch(const WfArgs &a, cudaStream_t s) {
+  const int grid = (a.items + WNW - 1) / WNW;
+  if (a.g.gj0 & 1) {
+    wf_blocks_per_sm<WM, 1>();
+    k_sor_wf<WM, 1><<<grid, WNT, wf_smem<WM>(), s>>>(a);
+  } else {
+    wf_blocks_per_sm<WM, 0>();
+    k_sor_wf<WM, 0><<<grid, WNT, wf_smem<WM>(), s>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int wf_box_rows(int m) { return 2 * m + 2; }
+
+// Strip / segment plan: segments of 64 rows (measured best on 8192^2 among
+// 48..512: short segments balance the slower body / edge items across the
+// waves; the 4 WM halo rows per segment cost ~12 %).  IBM_WF_ROWS overrides
+// the length for tuning; it is rounded up to even so colours stay compile-time.
+void wf_plan(WfArgs &a, int m) {
+  const int ow = 64 - 4 * m;
+  a.strips = (a.g.ni + ow - 1) / ow;
+  int L = 64;
+  if (const char *e = std::getenv("IBM_WF_ROWS")) {
+    const int v = std::atoi(e);
+    if (v > 0) L = v;
+  }
+  if (L < 2) L = 2;
+  L = (L + 1) & ~1;
+  a.L = L;
+  a.segs = (a.g.nj + L - 1) / L;
+  a.items = a.strips * a.segs;
+}
+
+cudaError_t launch_sor_wf(const WfArgs &a, int m, cudaStream_t s) {
+  switch (m) {
+    case 2: return wf_launch<2>(a, s);
+    case 3: return wf_launch<3>(a, s);
+    case 4: return wf_launch<4>(a, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace ibm

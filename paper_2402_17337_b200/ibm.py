@@ -45,7 +45,7 @@ class ibm_config(C.Structure):
                 ("omega_uv", C.c_double), ("tol_uv", C.c_double), ("maxit_uv", C.c_int),
                 ("check_every", C.c_int), ("rank", C.c_int), ("nranks", C.c_int),
                 ("nccl_id", C.c_void_p), ("device", C.c_int), ("sor_batch", C.c_int),
-                ("loopback", C.c_int)]
+                ("loopback", C.c_int), ("sor_fuse", C.c_int)]
 
 
 class ibm_step_stats(C.Structure):
@@ -103,7 +103,7 @@ def _check(func, st, ctx=None, ok=(IBM_OK,)):
 
 def make_config(xn, yn, Re, dt, omega_p=1.5, tol_p=1e-6, maxit_p=10000, omega_uv=1.2, tol_uv=1e-8,
                 maxit_uv=1000, check_every=1, rank=0, nranks=1, nccl_id=None, device=0, sor_batch=0,
-                loopback=False):
+                loopback=False, sor_fuse=0):
     xn = np.ascontiguousarray(xn, dtype=np.float64)
     yn = np.ascontiguousarray(yn, dtype=np.float64)
     cfg = ibm_config()
@@ -119,6 +119,7 @@ def make_config(xn, yn, Re, dt, omega_p=1.5, tol_p=1e-6, maxit_p=10000, omega_uv
         idbuf = C.create_string_buffer(bytes(nccl_id), 128)
         cfg.nccl_id = C.cast(idbuf, C.c_void_p)
     cfg.device, cfg.sor_batch, cfg.loopback = device, sor_batch, int(bool(loopback))
+    cfg.sor_fuse = int(sor_fuse)
     cfg._keep = (xn, yn, idbuf)  # keep host arrays alive for the call
     return cfg
 
