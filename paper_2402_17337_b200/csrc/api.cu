@@ -245,12 +245,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 2-D map over a family array incl. its ghost rows: dim0 = columns, dim1 = stored
 // rows; elements outside are zero-filled by the TMA unit
-bool make_map(CUtensorMap *m, double *base, const Geo &g, int box_h) {
+bool make_map(CUtensorMap *m, double *base, const Geo &g, int box_h, int box_w = kSorBoxW) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {(cuuint64_t)g.ni, (cuuint64_t)(g.nj + 2 * kGhost)};
   cuuint64_t strides[1] = {(cuuint64_t)g.pitch * sizeof(double)};
-  cuuint32_t box[2] = {(cuuint32_t)kSorBoxW, (cuuint32_t)box_h};
+  cuuint32_t box[2] = {(cuuint32_t)box_w, (cuuint32_t)box_h};
   cuuint32_t es[2] = {1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -294,9 +294,9 @@ bool make_coef_maps(Ctx &c) {
 bool make_maps(Slab &s, int wf_m) {
   bool ok = true;
   if (wf_m >= 2) {
-    ok = ok && make_map(&s.tm_wphi[0], s.phi[0], s.gp, wf_box_rows(wf_m));
-    ok = ok && make_map(&s.tm_wphi[1], s.phi[1], s.gp, wf_box_rows(wf_m));
-    ok = ok && make_map(&s.tm_wbp, s.bp, s.gp, wf_box_rows(wf_m));
+    ok = ok && make_map(&s.tm_wphi[0], s.phi[0], s.gp, wf_box_rows(wf_m), wf_box_cols());
+    ok = ok && make_map(&s.tm_wphi[1], s.phi[1], s.gp, wf_box_rows(wf_m), wf_box_cols());
+    ok = ok && make_map(&s.tm_wbp, s.bp, s.gp, wf_box_rows(wf_m), wf_box_cols());
   }
   for (int q = 0; q < 2; ++q) {
     ok = ok && make_map(&s.tm_phi[q], s.phi[q], s.gp, kSorBoxHx);

@@ -168,6 +168,7 @@ constexpr int kSorTileX = 60, kSorTileY = 16;
 void launch_sor_iteration(const SorArgs &a, cudaStream_t st, int grid);
 // temporally blocked Poisson pass: rows of the TMA box, segment length, launch
 int wf_box_rows(int m);
+int wf_box_cols();
 void wf_plan(WfArgs &a, int m);
 cudaError_t launch_sor_wf(const WfArgs &a, int m, cudaStream_t st);
 void launch_sor_check(SorCtl *ctl, const unsigned long long *rho_bits, int k, int maxit, int check_every,

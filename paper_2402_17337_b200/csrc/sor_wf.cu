@@ -27,6 +27,7 @@
 // reciprocals; the rest (domain edges, body, stretched rows) the predicated one.
 //
 // Arithmetic: identical to sor.cu (R13).
+#include <climits>
 #include <cstdlib>
 #include <type_traits>
 #include <utility>
@@ -41,11 +42,16 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr int WNW = 4;  // warps per CTA (independent work items)
 constexpr int WNT = 32 * WNW;
 constexpr int WNSTG = 2;  // stages per warp
+#ifndef WF_NS
+#define WF_NS 1
+#endif
+constexpr int NS = WF_NS;   // column pairs per lane: lane l holds pairs l + 32 st
+constexpr int SC = 64 * NS;  // stored columns per strip
 
 template <int WM>
 struct __align__(128) WfStage {
-  double x[2 * WM + 2][64];
-  double b[2 * WM + 2][64];
+  double x[2 * WM + 2][SC];
+  double b[2 * WM + 2][SC];
 };
 template <int WM>
 constexpr size_t wf_smem() {
@@ -60,42 +66,69 @@ constexpr int wf_min_blocks() {
   return (int)((220u * 1024u) / wf_smem<WM>()) < WF_MINB ? (int)((220u * 1024u) / wf_smem<WM>()) : WF_MINB;
 }
 
-// Per-lane column data of the two columns gi = i0 + 2l + e.
+// Per-lane column data of the columns gi = i0 + 2 (l + 32 st) + e.
 struct WfCols {
-  double aE[2], aW[2], sEW[2], cD[2], aPu[2], yu[2];
-  bool in[2];  // column inside the family's updatable range
+  double aE[NS][2], aW[NS][2], sEW[NS][2], cD[NS][2], aPu[NS][2], yu[NS][2];
+  bool in[NS][2];  // column inside the family's updatable range
 };
 
-// One node update of the check-free path: element E of window slot Q.  EDGE:
-// the strip reaches past the family's columns; lanes outside keep their value.
-template <int W, int Q, int E, bool EDGE>
-__device__ __forceinline__ void wf_fast(double2 (&X)[W], const double2 (&B)[W], const WfCols &C, double aN,
-                                        double aS, double omega, double omc, bool own, unsigned long long &tmax) {
-  constexpr int QN = (Q + 1) % W, QS = (Q + W - 1) % W;
+// Horizontal neighbour outside the pair for element E of window slot Q of every
+// pair set: E = 0 -> W from pair p-1 (.y); E = 1 -> E from pair p+1 (.x).  Pair
+// 31 / 32 cross between the sets; the strip's outermost neighbours are junk
+// (halo columns, never stored or counted).
+template <int W, int Q, int E>
+__device__ __forceinline__ void wf_nb(const double2 (&X)[NS][W], double (&nb)[NS]) {
   const int l = threadIdx.x & 31;
-  double xE, xW;
   if (E == 0) {
-    xW = __shfl_sync(FULL, X[Q].y, (l + 31) & 31);
-    xE = X[Q].y;
+    const double t0 = __shfl_sync(FULL, X[0][Q].y, (l + 31) & 31);
+    nb[0] = t0;
+    if (NS == 2) {
+      const double t1 = __shfl_sync(FULL, X[NS - 1][Q].y, (l + 31) & 31);
+      nb[NS - 1] = (l == 0) ? t0 : t1;
+    }
   } else {
-    xW = X[Q].x;
-    xE = __shfl_sync(FULL, X[Q].x, (l + 1) & 31);
+    const double t0 = __shfl_sync(FULL, X[0][Q].x, (l + 1) & 31);
+    if (NS == 2) {
+      const double t1 = __shfl_sync(FULL, X[NS - 1][Q].x, (l + 1) & 31);
+      nb[0] = (l == 31) ? t1 : t0;
+      nb[NS - 1] = t1;
+    } else {
+      nb[0] = t0;
+    }
   }
-  const double xo = rd(X[Q], E), xN = rd(X[QN], E), xS = rd(X[QS], E);
-  const double sm = __fma_rn(C.aE[E], xE, C.aW[E] * xW) + __fma_rn(aN, xN, aS * xS);
-  const double gs = (rd(B[Q], E) + sm) * C.yu[E];
-  const double xn = __fma_rn(omc, xo, omega * gs);
-  wr(X[Q], E, (!EDGE || C.in[E]) ? xn : xo);
-  const unsigned long long e = (unsigned long long)__double_as_longlong(fabs(gs - xo));
-  tmax = (own && e > tmax) ? e : tmax;
+}
+
+// One node update of the check-free path per pair set: element E of window
+// slot Q.  EDGE: the strip reaches past the family's columns; cells outside keep
+// their value and are not counted.
+template <int W, int Q, int E, bool EDGE>
+__device__ __forceinline__ void wf_fast(double2 (&X)[NS][W], const double2 (&B)[NS][W], const WfCols &C, double aN,
+                                        double aS, double omega, double omc, bool own,
+                                        unsigned long long (&tmax)[NS]) {
+  constexpr int QN = (Q + 1) % W, QS = (Q + W - 1) % W;
+  double nb[NS];
+  wf_nb<W, Q, E>(X, nb);
+#pragma unroll
+  for (int st = 0; st < NS; ++st) {
+    const double xE = E ? nb[st] : X[st][Q].y;
+    const double xW = E ? X[st][Q].x : nb[st];
+    const double xo = rd(X[st][Q], E), xN = rd(X[st][QN], E), xS = rd(X[st][QS], E);
+    const double sm = __fma_rn(C.aE[st][E], xE, C.aW[st][E] * xW) + __fma_rn(aN, xN, aS * xS);
+    const double gs = (rd(B[st][Q], E) + sm) * C.yu[st][E];
+    const double xn = __fma_rn(omc, xo, omega * gs);
+    wr(X[st][Q], E, (!EDGE || C.in[st][E]) ? xn : xo);
+    // |gs - xo| as a bit pattern: clearing the sign bit is fabs (integer pipe)
+    const unsigned long long e = (unsigned long long)__double_as_longlong(gs - xo) & 0x7fffffffffffffffull;
+    tmax[st] = ((!EDGE || C.in[st][E]) && own && e > tmax[st]) ? e : tmax[st];
+  }
 }
 
 // One node update of the predicated path (domain edges, body flags, arbitrary
 // row coefficients): the same per-cell logic as sor.cu's boundary tiles.
 template <int W, int Q, int E>
-__device__ __forceinline__ void wf_slow(double2 (&X)[W], const double2 (&B)[W], const WfCols &C, const WfArgs &A,
-                                        int r, int gi, bool hasf, double omega, double omc, bool own,
-                                        unsigned long long &tmax) {
+__device__ __forceinline__ void wf_slow(double2 (&X)[NS][W], const double2 (&B)[NS][W], const WfCols &C,
+                                        const WfArgs &A, int r, int i0, bool hasf, double omega, double omc, bool own,
+                                        unsigned long long (&tmax)[NS]) {
   constexpr int QN = (Q + 1) % W, QS = (Q + W - 1) % W;
   const int l = threadIdx.x & 31;
   const int gj = A.g.gj0 + r;
@@ -104,34 +137,35 @@ __device__ __forceinline__ void wf_slow(double2 (&X)[W], const double2 (&B)[W], 
     cN = A.cN[gj];
     cS = A.cS[gj];
   }
-  bool u = gi >= A.ui0 && gi < A.ui1 && gj >= A.uj0 && gj < A.uj1;
-  uint8_t fl = 0;
-  if (hasf && u) fl = A.flag[A.g.off(gi, r)];
-  u = u && !(fl & PF_INACTIVE);
-  double aE = C.aE[E], aW = C.aW[E], aN = cN, aS = cS, aP;
-  if (fl) {
-    aE = (fl & PF_E) ? 0.0 : aE;
-    aW = (fl & PF_W) ? 0.0 : aW;
-    aN = (fl & PF_N) ? 0.0 : aN;
-    aS = (fl & PF_S) ? 0.0 : aS;
-    aP = ((aE + aW) + (aN + aS)) + C.cD[E];
-  } else {
-    aP = (C.sEW[E] + (cN + cS)) + C.cD[E];
-  }
-  double xE, xW;
-  if (E == 0) {
-    xW = __shfl_sync(FULL, X[Q].y, (l + 31) & 31);
-    xE = X[Q].y;
-  } else {
-    xW = X[Q].x;
-    xE = __shfl_sync(FULL, X[Q].x, (l + 1) & 31);
-  }
-  const double xo = rd(X[Q], E), xN = rd(X[QN], E), xS = rd(X[QS], E);
-  const double sm = __fma_rn(aE, xE, aW * xW) + __fma_rn(aN, xN, aS * xS);
-  const double gs = (rd(B[Q], E) + sm) * __drcp_rn(aP);
-  if (u) {
-    wr(X[Q], E, __fma_rn(omc, xo, omega * gs));
-    if (own) tmax = umax64(tmax, (unsigned long long)__double_as_longlong(fabs(gs - xo)));
+  double nb[NS];
+  wf_nb<W, Q, E>(X, nb);
+#pragma unroll
+  for (int st = 0; st < NS; ++st) {
+    const int gi = i0 + 2 * (l + 32 * st) + E;
+    bool u = gi >= A.ui0 && gi < A.ui1 && gj >= A.uj0 && gj < A.uj1;
+    uint8_t fl = 0;
+    if (hasf && u) fl = A.flag[A.g.off(gi, r)];
+    u = u && !(fl & PF_INACTIVE);
+    double aE = C.aE[st][E], aW = C.aW[st][E], aN = cN, aS = cS, aP;
+    if (fl) {
+      aE = (fl & PF_E) ? 0.0 : aE;
+      aW = (fl & PF_W) ? 0.0 : aW;
+      aN = (fl & PF_N) ? 0.0 : aN;
+      aS = (fl & PF_S) ? 0.0 : aS;
+      aP = ((aE + aW) + (aN + aS)) + C.cD[st][E];
+    } else {
+      aP = (C.sEW[st][E] + (cN + cS)) + C.cD[st][E];
+    }
+    const double xE = E ? nb[st] : X[st][Q].y;
+    const double xW = E ? X[st][Q].x : nb[st];
+    const double xo = rd(X[st][Q], E), xN = rd(X[st][QN], E), xS = rd(X[st][QS], E);
+    const double sm = __fma_rn(aE, xE, aW * xW) + __fma_rn(aN, xN, aS * xS);
+    const double gs = (rd(B[st][Q], E) + sm) * __drcp_rn(aP);
+    if (u) {
+      wr(X[st][Q], E, __fma_rn(omc, xo, omega * gs));
+      if (own)
+        tmax[st] = umax64(tmax[st], (unsigned long long)__double_as_longlong(gs - xo) & 0x7fffffffffffffffull);
+    }
   }
 }
 
@@ -161,49 +195,55 @@ __device__ __forceinline__ void sfor(F &&f) {
 
 // The W steps of one chunk (window slot q = row rb + q).  MODE 2: check-free
 // interior strip; 1: check-free edge strip; 0: predicated.  OWN: every row the
-// chunk touches is owned by the item (residual and stores need only the lane
-// test).  rb is even and W is even, so the slot and the colour element of every
-// half-sweep are compile-time constants.
+// chunk touches is owned by the item (the residual needs no row test; halo
+// lanes are dropped once per item).  rb is even and W is even, so the slot and
+// the colour element of every half-sweep are compile-time constants.
 template <int WM, int TP, int MODE, bool OWN>
-__device__ __forceinline__ void wf_chunk(double2 (&X)[2 * WM + 2], double2 (&B)[2 * WM + 2],
+__device__ __forceinline__ void wf_chunk(double2 (&X)[NS][2 * WM + 2], double2 (&B)[NS][2 * WM + 2],
                                          const WfStage<WM> &S, const WfCols &C, const WfArgs &A, int rb, int j0,
-                                         int j1, int i0, bool lane_own, bool hasf, double cN0, double cS0,
-                                         unsigned long long (&tmax)[WM]) {
+                                         int j1, int i0, const bool (&lane_own)[NS], bool hasf, double cN0,
+                                         double cS0, unsigned long long (&tmax)[WM][NS]) {
   constexpr int W = 2 * WM + 2;
   const int l = threadIdx.x & 31;
   const double omega = A.omega, omc = A.omc;
   const long pitch = A.g.pitch;
-  // stored row rb + q - 2WM of this lane's pair
+  // stored row rb + q - 2WM of this lane's first pair (the second is 64 columns on)
   double *const ob = A.xout + (long)(rb - 2 * WM + kGhost) * pitch + (i0 + 2 * l);
-  const bool pair_in = MODE == 2 || i0 + 2 * l + 1 < A.g.ni;
   sfor<W>([&](auto qc) {
     constexpr int q = decltype(qc)::value;
-    X[q] = *reinterpret_cast<const double2 *>(&S.x[q][2 * l]);
-    B[q] = *reinterpret_cast<const double2 *>(&S.b[q][2 * l]);
+#pragma unroll
+    for (int st = 0; st < NS; ++st) {
+      X[st][q] = *reinterpret_cast<const double2 *>(&S.x[q][2 * (l + 32 * st)]);
+      B[st][q] = *reinterpret_cast<const double2 *>(&S.b[q][2 * (l + 32 * st)]);
+    }
     sfor<2 * WM>([&](auto hc) {
       constexpr int h = decltype(hc)::value;
       constexpr int Q = ((q - 1 - h) % W + W) % W;  // slot of row rb + q - 1 - h
       constexpr int E = (TP + Q + h) & 1;           // red (h even): (i + j) even
       const int r = rb + q - 1 - h;
-      const bool own = OWN ? lane_own : (lane_own && r >= j0 && r < j1);
+      const bool own = OWN ? true : (r >= j0 && r < j1);
       if constexpr (MODE > 0)
         wf_fast<W, Q, E, MODE == 1>(X, B, C, cN0, cS0, omega, omc, own, tmax[h / 2]);
       else
-        wf_slow<W, Q, E>(X, B, C, A, r, i0 + 2 * l + E, hasf, omega, omc, own, tmax[h / 2]);
+        wf_slow<W, Q, E>(X, B, C, A, r, i0, hasf, omega, omc, own, tmax[h / 2]);
     });
     // row rb + q - 2WM has received its last half-sweep: store the owned columns
     const int ro = rb + q - 2 * WM;
-    const double2 v = X[((q - 2 * WM) % W + W) % W];
-    const bool st = OWN ? lane_own : (lane_own && ro >= j0 && ro < j1);
-    st_pred(st && pair_in, ob + q * pitch, v);
-    if (MODE < 2) st_pred1(st && !pair_in, ob + q * pitch, v.x);
+    const bool rowin = OWN || (ro >= j0 && ro < j1);
+#pragma unroll
+    for (int st = 0; st < NS; ++st) {
+      const double2 v = X[st][((q - 2 * WM) % W + W) % W];
+      const bool pair_in = MODE == 2 || i0 + 2 * (l + 32 * st) + 1 < A.g.ni;
+      st_pred(rowin && lane_own[st] && pair_in, ob + q * pitch + 64 * st, v);
+      if (MODE < 2) st_pred1(rowin && lane_own[st] && !pair_in, ob + q * pitch + 64 * st, v.x);
+    }
   });
 }
 
 template <int WM, int TP>
 __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __grid_constant__ WfArgs A) {
-  constexpr int W = 2 * WM + 2, OW = 64 - 4 * WM;
-  constexpr unsigned kBytes = 2u * W * 64 * 8;
+  constexpr int W = 2 * WM + 2, OW = SC - 4 * WM;
+  constexpr unsigned kBytes = 2u * W * SC * 8;
   if (*(volatile int *)&A.ctl->k_done >= 0) return;  // converged at an earlier iteration
   extern __shared__ __align__(1024) unsigned char smraw[];
   __shared__ unsigned long long wmax[WNW][WM];
@@ -211,9 +251,11 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
   WfStage<WM> *st = reinterpret_cast<WfStage<WM> *>(smraw) + w * WNSTG;
   unsigned long long *bar =
       reinterpret_cast<unsigned long long *>(smraw + (size_t)WNW * WNSTG * sizeof(WfStage<WM>)) + w * WNSTG;
-  unsigned long long tmax[WM];
+  unsigned long long tmax[WM][NS];
 #pragma unroll
-  for (int i = 0; i < WM; ++i) tmax[i] = 0ull;
+  for (int i = 0; i < WM; ++i)
+#pragma unroll
+    for (int s = 0; s < NS; ++s) tmax[i][s] = 0ull;
   const int item = blockIdx.x * WNW + w;
   if (item < A.items) {
     const Geo &g = A.g;
@@ -233,46 +275,58 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
       }
     }
     __syncwarp();
-    const bool lane_own = l >= WM && l <= 31 - WM && i0 + 2 * l < g.ni;
-    const bool interior = i0 >= A.ui0 && i0 + 64 <= A.ui1;
-    const bool boxstrip = !A.box.empty() && i0 < A.box.i1 && i0 + 64 > A.box.i0;
+    bool lane_own[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const int p = l + 32 * s;
+      lane_own[s] = p >= WM && p <= 32 * NS - 1 - WM && i0 + 2 * p < g.ni;
+    }
+    const bool interior = i0 >= A.ui0 && i0 + SC <= A.ui1;
+    const bool boxstrip = !A.box.empty() && i0 < A.box.i1 && i0 + SC > A.box.i0;
     // column coefficients (0 outside the family) and the reference row of the segment
     const int jr = min(max(g.gj0 + j0 + A.L / 2, 1), g.NJ - 2);
     const double cN0 = A.cN[jr], cS0 = A.cS[jr];
     WfCols C;
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int gi = i0 + 2 * l + e;
-      const bool in = gi >= 0 && gi < g.ni;
-      const double cE = in ? A.cE[gi] : 0.0, cW = in ? A.cW[gi] : 0.0;
-      C.cD[e] = in ? A.cD[gi] : 0.0;
-      C.aE[e] = cE;
-      C.aW[e] = cW;
-      C.sEW[e] = cE + cW;
-      C.aPu[e] = (C.sEW[e] + (cN0 + cS0)) + C.cD[e];
-      C.yu[e] = __drcp_rn(C.aPu[e]);
-      C.in[e] = gi >= A.ui0 && gi < A.ui1;
-    }
-    double2 X[W], B[W];
+    for (int s = 0; s < NS; ++s)
 #pragma unroll
-    for (int q = 0; q < W; ++q) X[q] = B[q] = make_double2(0.0, 0.0);
-    // row test of chunk c (rows rb-2WM .. rb+W-2), prefetched one chunk ahead
-    auto row_ok = [&](int c, double &pn, double &ps) -> bool {
-      const int r = rs + c * W - 2 * WM + l, gj = g.gj0 + r;
-      const bool in = l <= 4 * WM && gj >= A.uj0 && gj < A.uj1;
-      pn = in ? A.cN[gj] : 0.0;
-      ps = in ? A.cS[gj] : 0.0;
-      return in && !(boxstrip && r >= A.box.j0 && r < A.box.j1);
-    };
-    double pn, ps;
-    bool pin = row_ok(0, pn, ps);
+      for (int e = 0; e < 2; ++e) {
+        const int gi = i0 + 2 * (l + 32 * s) + e;
+        const bool in = gi >= 0 && gi < g.ni;
+        const double cE = in ? A.cE[gi] : 0.0, cW = in ? A.cW[gi] : 0.0;
+        C.cD[s][e] = in ? A.cD[gi] : 0.0;
+        C.aE[s][e] = cE;
+        C.aW[s][e] = cW;
+        C.sEW[s][e] = cE + cW;
+        C.aPu[s][e] = (C.sEW[s][e] + (cN0 + cS0)) + C.cD[s][e];
+        C.yu[s][e] = __drcp_rn(C.aPu[s][e]);
+        C.in[s][e] = gi >= A.ui0 && gi < A.ui1;
+      }
+    double2 X[NS][W], B[NS][W];
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+#pragma unroll
+      for (int q = 0; q < W; ++q) X[s][q] = B[s][q] = make_double2(0.0, 0.0);
+    // Irregular rows of the item (outside the family, in the body box, or with
+    // row coefficients other than the reference): the chunks whose rows
+    // rb-2WM .. rb+W-2 meet [irr0, irr1] take the predicated path.
+    int irr0 = INT_MAX, irr1 = INT_MIN;
+    for (int r = rs - 2 * WM + l; r <= rs + nch * W - 2; r += 32) {
+      const int gj = g.gj0 + r;
+      const bool reg = gj >= A.uj0 && gj < A.uj1 && !(boxstrip && r >= A.box.j0 && r < A.box.j1) &&
+                       A.cN[gj] == cN0 && A.cS[gj] == cS0;
+      if (!reg) {
+        irr0 = min(irr0, r);
+        irr1 = max(irr1, r);
+      }
+    }
+    irr0 = __reduce_min_sync(FULL, irr0);
+    irr1 = __reduce_max_sync(FULL, irr1);
     for (int c = 0; c < nch; ++c) {
       const int s = c % WNSTG;
       const int rb = rs + c * W;
-      const bool good = l > 4 * WM || (pin && pn == cN0 && ps == cS0);
-      const bool fast = __all_sync(FULL, good);
+      const bool fast = rb + W - 2 < irr0 || rb - 2 * WM > irr1;
       const bool hasf = boxstrip && rb + W - 2 >= A.box.j0 && rb - 2 * WM < A.box.j1;
-      if (c + 1 < nch) pin = row_ok(c + 1, pn, ps);
       mbar_wait_warp(&bar[s], (c / WNSTG) & 1);
       const bool ownall = rb - 2 * WM >= j0 && rb + W - 2 < j1;
       if (fast && interior && ownall)
@@ -293,11 +347,18 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
     }
   }
   // residual of each fused iteration: warp -> CTA -> atomicMax on its bit pattern
+  // (halo pairs accumulated recomputed cells: dropped here)
 #pragma unroll
   for (int i = 0; i < WM; ++i) {
+    unsigned long long t = 0ull;
 #pragma unroll
-    for (int off = 16; off; off >>= 1) tmax[i] = umax64(tmax[i], __shfl_xor_sync(FULL, tmax[i], off));
-    if (l == 0) wmax[w][i] = tmax[i];
+    for (int s = 0; s < NS; ++s) {
+      const int p = l + 32 * s;
+      if (p >= WM && p <= 32 * NS - 1 - WM) t = umax64(t, tmax[i][s]);
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) t = umax64(t, __shfl_xor_sync(FULL, t, off));
+    if (l == 0) wmax[w][i] = t;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -358,13 +419,14 @@ cudaError_t wf_launch(const WfArgs &a, cudaStream_t s) {
 }  // namespace
 
 int wf_box_rows(int m) { return 2 * m + 2; }
+int wf_box_cols() { return SC; }
 
 // Strip / segment plan: segments of 64 rows (measured best on 8192^2 among
 // 48..512: short segments balance the slower body / edge items across the
 // waves; the 4 WM halo rows per segment cost ~12 %).  IBM_WF_ROWS overrides
 // the length for tuning; it is rounded up to even so colours stay compile-time.
 void wf_plan(WfArgs &a, int m) {
-  const int ow = 64 - 4 * m;
+  const int ow = SC - 4 * m;
   a.strips = (a.g.ni + ow - 1) / ow;
   int L = 64;
   if (const char *e = std::getenv("IBM_WF_ROWS")) {
