@@ -88,7 +88,7 @@ typedef struct {
                                    reductions by device copies (decomposition test mode; rank
                                    ignored, get/set_fields cover the whole grid) */
     int sor_fuse;               /* Poisson red-black iterations fused per HBM pass (temporal
-                                   blocking): 0 = default (2), 1 = one iteration
+                                   blocking): 0 = default (3), 1 = one iteration
                                    per pass, 2..4; slab-decomposed runs use 1 */
 } ibm_config;
 

@@ -296,14 +296,14 @@ typedef struct {
 /* Runs red-black SOR on nsys independent systems jointly: one iteration = red
  * sweep of every system, then black sweep of every system; rho_k = max over all
  * updates of |gs - x_old|.  Node update (R2, R13):
- *   s = fma(aE, xE, aW*xW) + fma(aN, xN, aS*xS);  gs = (b + s) * (1/aP);
- *   x = fma(1-omega, x_old, omega*gs).  1/aP is the correctly rounded reciprocal
- *   (one IEEE division), then one IEEE multiplication -- reading R13.  Colour red = (i+j) even.  Returns iterations; status
+ *   n = fma(aN, xN, fma(aE, xE, fma(aW, xW, fma(aS, xS, b))));  gs = n * (1/aP);
+ *   d = gs - x_old;  x = fma(omega, d, x_old) (= (1-omega) x_old + omega gs);  e = |d|.
+ *   fma is C99 fma (one rounding); 1/aP is the correctly rounded reciprocal (one
+ *   IEEE division) -- reading R13.  Colour red = (i+j) even.  Returns iterations; status
  * ORC_ERR_DIVERGED if rho is NaN, ORC_WARN_NOCONV if maxit reached above tol. */
 static int sor_run(int nsys, sor_sys *sys, double omega, double tol, int maxit,
                    int check_every, double *rho_out, int *status)
 {
-    double omc = 1.0 - omega;
     double rho = 0.0;
     int k;
     *status = ORC_OK;
@@ -321,13 +321,16 @@ static int sor_run(int nsys, sor_sys *sys, double omega, double tol, int maxit,
                         double xW = fv_at(S->x, S->ni, S->nj, i - 1, j);
                         double xN = fv_at(S->x, S->ni, S->nj, i, j + 1);
                         double xS = fv_at(S->x, S->ni, S->nj, i, j - 1);
-                        /* R13: two explicit fused multiply-adds (C99 fma, one rounding each) */
-                        double sum = fma(S->aE[id], xE, S->aW[id] * xW) + fma(S->aN[id], xN, S->aS[id] * xS);
+                        /* R13: b + sum of the neighbour terms as a chain of fused multiply-adds
+                         * (C99 fma, one rounding each), S, W, E, N */
+                        double num = fma(S->aN[id], xN, fma(S->aE[id], xE, fma(S->aW[id], xW,
+                                         fma(S->aS[id], xS, S->b[id]))));
                         double rcp = 1.0 / S->aP[id];
-                        double gs = (S->b[id] + sum) * rcp;
+                        double gs = num * rcp;
                         double xo = S->x[id];
-                        double e = fabs(gs - xo);
-                        S->x[id] = fma(omc, xo, omega * gs);
+                        double d = gs - xo;
+                        double e = fabs(d);
+                        S->x[id] = fma(omega, d, xo);
                         if (isnan(e) || isnan(rho)) rho = NAN;
                         else if (e > rho) rho = e;
                     }

@@ -751,7 +751,7 @@ int ibm_init(const ibm_config *cfg, void *d_workspace, size_t bytes, void *cuda_
   c.hint_uv = 16;
   c.hint_p = 64;
   // temporal blocking of the Poisson pass needs 2 m halo rows: single slab only
-  c.wf_m = (cfg->loopback || cfg->nranks > 1) ? 1 : (cfg->sor_fuse == 0 ? 2 : cfg->sor_fuse);
+  c.wf_m = (cfg->loopback || cfg->nranks > 1) ? 1 : (cfg->sor_fuse == 0 ? 3 : cfg->sor_fuse);
   if (c.loopback)
     for (int r = 0; r < cfg->nranks; ++r) c.sl.push_back(make_slab(*cfg, r));
   else

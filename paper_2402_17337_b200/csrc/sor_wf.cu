@@ -41,7 +41,12 @@ namespace {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int WNW = 4;  // warps per CTA (independent work items)
 constexpr int WNT = 32 * WNW;
-constexpr int WNSTG = 2;  // stages per warp
+// stages per warp: 2 for m = 2, 3 for m >= 3 (measured: the deeper pass needs the
+// longer TMA lead; the shallower one loses a resident CTA with a third stage)
+template <int WM>
+__host__ __device__ constexpr int wf_nstg() {
+  return WM >= 3 ? 3 : 2;
+}
 #ifndef WF_NS
 #define WF_NS 1
 #endif
@@ -55,7 +60,7 @@ struct __align__(128) WfStage {
 };
 template <int WM>
 constexpr size_t wf_smem() {
-  return (size_t)WNW * WNSTG * sizeof(WfStage<WM>) + (size_t)WNW * WNSTG * sizeof(unsigned long long);
+  return (size_t)WNW * wf_nstg<WM>() * (sizeof(WfStage<WM>) + sizeof(unsigned long long));
 }
 #ifndef WF_MINB
 #define WF_MINB 3
@@ -113,12 +118,13 @@ __device__ __forceinline__ void wf_fast(double2 (&X)[NS][W], const double2 (&B)[
     const double xE = E ? nb[st] : X[st][Q].y;
     const double xW = E ? X[st][Q].x : nb[st];
     const double xo = rd(X[st][Q], E), xN = rd(X[st][QN], E), xS = rd(X[st][QS], E);
-    const double sm = __fma_rn(C.aE[st][E], xE, C.aW[st][E] * xW) + __fma_rn(aN, xN, aS * xS);
-    const double gs = (rd(B[st][Q], E) + sm) * C.yu[st][E];
-    const double xn = __fma_rn(omc, xo, omega * gs);
+    const double nm =
+        __fma_rn(aN, xN, __fma_rn(C.aE[st][E], xE, __fma_rn(C.aW[st][E], xW, __fma_rn(aS, xS, rd(B[st][Q], E)))));
+    const double d = nm * C.yu[st][E] - xo;  // gs - x_old (--fmad=false: two roundings)
+    const double xn = __fma_rn(omega, d, xo);
     wr(X[st][Q], E, (!EDGE || C.in[st][E]) ? xn : xo);
     // |gs - xo| as a bit pattern: clearing the sign bit is fabs (integer pipe)
-    const unsigned long long e = (unsigned long long)__double_as_longlong(gs - xo) & 0x7fffffffffffffffull;
+    const unsigned long long e = (unsigned long long)__double_as_longlong(d) & 0x7fffffffffffffffull;
     tmax[st] = ((!EDGE || C.in[st][E]) && own && e > tmax[st]) ? e : tmax[st];
   }
 }
@@ -159,12 +165,11 @@ __device__ __forceinline__ void wf_slow(double2 (&X)[NS][W], const double2 (&B)[
     const double xE = E ? nb[st] : X[st][Q].y;
     const double xW = E ? X[st][Q].x : nb[st];
     const double xo = rd(X[st][Q], E), xN = rd(X[st][QN], E), xS = rd(X[st][QS], E);
-    const double sm = __fma_rn(aE, xE, aW * xW) + __fma_rn(aN, xN, aS * xS);
-    const double gs = (rd(B[st][Q], E) + sm) * __drcp_rn(aP);
+    const double nm = __fma_rn(aN, xN, __fma_rn(aE, xE, __fma_rn(aW, xW, __fma_rn(aS, xS, rd(B[st][Q], E)))));
+    const double d = nm * __drcp_rn(aP) - xo;
     if (u) {
-      wr(X[st][Q], E, __fma_rn(omc, xo, omega * gs));
-      if (own)
-        tmax[st] = umax64(tmax[st], (unsigned long long)__double_as_longlong(gs - xo) & 0x7fffffffffffffffull);
+      wr(X[st][Q], E, __fma_rn(omega, d, xo));
+      if (own) tmax[st] = umax64(tmax[st], (unsigned long long)__double_as_longlong(d) & 0x7fffffffffffffffull);
     }
   }
 }
@@ -242,15 +247,15 @@ __device__ __forceinline__ void wf_chunk(double2 (&X)[NS][2 * WM + 2], double2 (
 
 template <int WM, int TP>
 __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __grid_constant__ WfArgs A) {
-  constexpr int W = 2 * WM + 2, OW = SC - 4 * WM;
+  constexpr int W = 2 * WM + 2, OW = SC - 4 * WM, NSTG = wf_nstg<WM>();
   constexpr unsigned kBytes = 2u * W * SC * 8;
   if (*(volatile int *)&A.ctl->k_done >= 0) return;  // converged at an earlier iteration
   extern __shared__ __align__(1024) unsigned char smraw[];
   __shared__ unsigned long long wmax[WNW][WM];
   const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
-  WfStage<WM> *st = reinterpret_cast<WfStage<WM> *>(smraw) + w * WNSTG;
+  WfStage<WM> *st = reinterpret_cast<WfStage<WM> *>(smraw) + w * NSTG;
   unsigned long long *bar =
-      reinterpret_cast<unsigned long long *>(smraw + (size_t)WNW * WNSTG * sizeof(WfStage<WM>)) + w * WNSTG;
+      reinterpret_cast<unsigned long long *>(smraw + (size_t)WNW * NSTG * sizeof(WfStage<WM>)) + w * NSTG;
   unsigned long long tmax[WM][NS];
 #pragma unroll
   for (int i = 0; i < WM; ++i)
@@ -266,9 +271,9 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
     const int rs = j0 - 2 * WM;       // first streamed row
     const int nch = ((j1 - j0) + 4 * WM + W - 1) / W;
     if (l == 0) {
-      for (int s = 0; s < WNSTG; ++s) mbar_init(&bar[s], 1);
+      for (int s = 0; s < NSTG; ++s) mbar_init(&bar[s], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      for (int c = 0; c < WNSTG && c < nch; ++c) {
+      for (int c = 0; c < NSTG && c < nch; ++c) {
         mbar_expect_tx(&bar[c], kBytes);
         tma_load_2d(&st[c].x[0][0], &A.tmx, i0, rs + c * W + kGhost, &bar[c]);
         tma_load_2d(&st[c].b[0][0], &A.tmb, i0, rs + c * W + kGhost, &bar[c]);
@@ -323,11 +328,11 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
     irr0 = __reduce_min_sync(FULL, irr0);
     irr1 = __reduce_max_sync(FULL, irr1);
     for (int c = 0; c < nch; ++c) {
-      const int s = c % WNSTG;
+      const int s = c % NSTG;
       const int rb = rs + c * W;
       const bool fast = rb + W - 2 < irr0 || rb - 2 * WM > irr1;
       const bool hasf = boxstrip && rb + W - 2 >= A.box.j0 && rb - 2 * WM < A.box.j1;
-      mbar_wait_warp(&bar[s], (c / WNSTG) & 1);
+      mbar_wait_warp(&bar[s], (c / NSTG) & 1);
       const bool ownall = rb - 2 * WM >= j0 && rb + W - 2 < j1;
       if (fast && interior && ownall)
         wf_chunk<WM, TP, 2, true>(X, B, st[s], C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax);
@@ -338,11 +343,11 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
       else
         wf_chunk<WM, TP, 0, false>(X, B, st[s], C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax);
       __syncwarp();
-      if (l == 0 && c + WNSTG < nch) {
+      if (l == 0 && c + NSTG < nch) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&bar[s], kBytes);
-        tma_load_2d(&st[s].x[0][0], &A.tmx, i0, rs + (c + WNSTG) * W + kGhost, &bar[s]);
-        tma_load_2d(&st[s].b[0][0], &A.tmb, i0, rs + (c + WNSTG) * W + kGhost, &bar[s]);
+        tma_load_2d(&st[s].x[0][0], &A.tmx, i0, rs + (c + NSTG) * W + kGhost, &bar[s]);
+        tma_load_2d(&st[s].b[0][0], &A.tmb, i0, rs + (c + NSTG) * W + kGhost, &bar[s]);
       }
     }
   }

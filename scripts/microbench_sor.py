@@ -13,7 +13,7 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
 pre = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 mp = int(sys.argv[3]) if len(sys.argv) > 3 else 300
 fuse = int(sys.argv[4]) if len(sys.argv) > 4 else 0
-m = fuse if fuse else 2
+m = fuse if fuse else 3
 cfg = I.cfg4(n=n, maxit_p=mp, maxit_uv=1000)
 g = P.Solver(cfg.xn, cfg.yn, sor_fuse=fuse, **cfg.solver_kwargs())
 g.set_body(*cfg.body_args())
