@@ -94,6 +94,19 @@ void slab_rows(int ny, int P, int r, int *j0, int *j1) {
   *j1 = *j0 + base + (r < rem ? 1 : 0);
 }
 
+// Row pitch in doubles: a multiple of 32 (256 B), plus 32 when that is a multiple
+// of 512 (4 KB): power-of-two row strides map the rows a wave of strips reads at
+// once onto the same DRAM channels (IBM_PITCH_PAD=0 disables, for measurement).
+long row_pitch(int n) {
+  long p = round_up(n, 32);
+  static const int pad = [] {
+    const char *e = std::getenv("IBM_PITCH_PAD");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (pad && p % 512 == 0) p += 32;
+  return p;
+}
+
 Slab make_slab(const ibm_config &cfg, int r) {
   Slab s;
   std::memset(&s, 0, sizeof(s));
@@ -101,9 +114,9 @@ Slab make_slab(const ibm_config &cfg, int r) {
   slab_rows(cfg.ny, cfg.nranks, r, &s.pj0, &s.pj1);
   const int nj = s.pj1 - s.pj0;
   const bool last = (r == cfg.nranks - 1);
-  s.gu = Geo{cfg.nx + 1, nj, s.pj0, cfg.ny, round_up(cfg.nx + 1, 32)};
-  s.gv = Geo{cfg.nx, nj + (last ? 1 : 0), s.pj0, cfg.ny + 1, round_up(cfg.nx, 32)};
-  s.gp = Geo{cfg.nx, nj, s.pj0, cfg.ny, round_up(cfg.nx, 32)};
+  s.gu = Geo{cfg.nx + 1, nj, s.pj0, cfg.ny, row_pitch(cfg.nx + 1)};
+  s.gv = Geo{cfg.nx, nj + (last ? 1 : 0), s.pj0, cfg.ny + 1, row_pitch(cfg.nx)};
+  s.gp = Geo{cfg.nx, nj, s.pj0, cfg.ny, row_pitch(cfg.nx)};
   s.bu = s.bv = s.bpb = BBox{0, 0, 0, 0};
   return s;
 }

@@ -426,14 +426,16 @@ cudaError_t wf_launch(const WfArgs &a, cudaStream_t s) {
 int wf_box_rows(int m) { return 2 * m + 2; }
 int wf_box_cols() { return SC; }
 
-// Strip / segment plan: segments of 64 rows (measured best on 8192^2 among
-// 48..512: short segments balance the slower body / edge items across the
-// waves; the 4 WM halo rows per segment cost ~12 %).  IBM_WF_ROWS overrides
-// the length for tuning; it is rounded up to even so colours stay compile-time.
+// Strip / segment plan: segments of L owned rows, L = 64 for m = 2 and 128 for
+// m >= 3 (measured on 8192^2 over 48..512: short segments balance the slower
+// body / edge items over the waves, but every segment recomputes 4m halo rows
+// and rounds its 2m+2-row chunks up, which costs more for deeper fusion;
+// scripts/gpu_wf_tune.sh).  IBM_WF_ROWS overrides L for tuning; it is rounded up
+// to even so colours stay compile-time.
 void wf_plan(WfArgs &a, int m) {
   const int ow = SC - 4 * m;
   a.strips = (a.g.ni + ow - 1) / ow;
-  int L = 64;
+  int L = m == 2 ? 64 : 128;
   if (const char *e = std::getenv("IBM_WF_ROWS")) {
     const int v = std::atoi(e);
     if (v > 0) L = v;
