@@ -13,7 +13,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
     python bench.py --steps 1 --warmup 0 --maxit-p 200 --no-e2e --no-cpu-baseline --no-clocks --sor-batch 256 > /dev/null 2>&1
 # full captures: the fused Poisson pass (k_sor_wf, 2 iterations per launch) ~120 iterations into the
 # first step, the one-iteration pass (--sor-fuse 1) likewise, and the other kernels
-ncu --set full --clock-control none --import-source on -k regex:k_sor_wf -s 60 -c 1 -o gpurun_out/prof_wf_${TAG} -f \
+ncu --set full --clock-control none --import-source on -k regex:k_sor_wf -s 40 -c 1 -o gpurun_out/prof_wf_${TAG} -f \
     python bench.py --steps 1 --warmup 0 --maxit-p 220 --no-e2e --no-cpu-baseline --no-clocks --sor-batch 256 > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_sor -s 205 -c 1 -o gpurun_out/prof_sor_${TAG} -f \
     python bench.py --steps 1 --warmup 0 --maxit-p 220 --no-e2e --no-cpu-baseline --no-clocks --sor-batch 256 --sor-fuse 1 > /dev/null 2>&1

@@ -107,13 +107,13 @@ tot = sum(v[1] for v in agg.values())
 lines = ["Launch list of `python bench.py --steps 1 --warmup 0 --maxit-p 200 --no-e2e --no-cpu-baseline` (one step,",
          "Poisson capped at 200 iterations) under `ncu --metrics gpu__time_duration.sum --clock-control none`.",
          "Cold-cache, serialised per-launch times: compare SHARES, not absolutes.  At maxit_p = 10^4 (the bench)",
-         "the fused Poisson pass k_sor_wf<2,0> repeats 5000 times per step, so its share approaches 100%.", "",
+         "the fused Poisson pass k_sor_wf<3,0> repeats ~3333 times per step, so its share approaches 100%.", "",
          "%-28s %6s %12s %10s %7s" % ("kernel", "n", "total us", "avg us", "share")]
 for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
     lines.append("%-28s %6d %12.1f %10.1f %6.1f%%" % (k, n, t, t / n, 100 * t / tot))
 open(os.path.join(P, "%s_launches.txt" % rnd), "w").write("\n".join(lines) + "\n")
 
-for kind, title in (("wf", "Fused Poisson pass (k_sor_wf<2,0>: 2 red-black iterations per launch), 8192^2 foil, "
+for kind, title in (("wf", "Fused Poisson pass (k_sor_wf<3,0>: 3 red-black iterations per launch), 8192^2 foil, "
                            "~120 iterations into step 1; per cell = per pass"),
                     ("sor", "One-iteration Poisson pass (k_sor<0,0>, --sor-fuse 1), 8192^2 foil, ~200 iterations into step 1"),
                     ("uvsor", "Velocity (Helmholtz) red-black SOR pass (k_sor<1,0>, u and v), 8192^2"),
