@@ -39,13 +39,20 @@ namespace ibm {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int WNW = 4;  // warps per CTA (independent work items)
+#ifndef WF_NW
+#define WF_NW 4
+#endif
+constexpr int WNW = WF_NW;  // warps per CTA (independent work items)
 constexpr int WNT = 32 * WNW;
 // stages per warp: 2 for m = 2, 3 for m >= 3 (measured: the deeper pass needs the
 // longer TMA lead; the shallower one loses a resident CTA with a third stage)
 template <int WM>
 __host__ __device__ constexpr int wf_nstg() {
+#ifdef WF_NSTG
+  return WF_NSTG;
+#else
   return WM >= 3 ? 3 : 2;
+#endif
 }
 #ifndef WF_NS
 #define WF_NS 1
@@ -73,7 +80,7 @@ constexpr int wf_min_blocks() {
 
 // Per-lane column data of the columns gi = i0 + 2 (l + 32 st) + e.
 struct WfCols {
-  double aE[NS][2], aW[NS][2], sEW[NS][2], cD[NS][2], aPu[NS][2], yu[NS][2];
+  double aE[NS][2], aW[NS][2], sEW[NS][2], cD[NS][2], yu[NS][2];
   bool in[NS][2];  // column inside the family's updatable range
 };
 
@@ -303,8 +310,7 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
         C.aE[s][e] = cE;
         C.aW[s][e] = cW;
         C.sEW[s][e] = cE + cW;
-        C.aPu[s][e] = (C.sEW[s][e] + (cN0 + cS0)) + C.cD[s][e];
-        C.yu[s][e] = __drcp_rn(C.aPu[s][e]);
+        C.yu[s][e] = __drcp_rn((C.sEW[s][e] + (cN0 + cS0)) + C.cD[s][e]);
         C.in[s][e] = gi >= A.ui0 && gi < A.ui1;
       }
     double2 X[NS][W], B[NS][W];
