@@ -40,7 +40,7 @@ import ibm_inputs as I  # noqa: E402
 
 METRIC = "Poisson+stencil grid-point updates/s"
 UNIT = "grid-point updates/s"
-BYTES_PER_POISSON_UPDATE = 24  # phi read + b read + phi write, fp64
+BYTES_PER_POISSON_UPDATE = 24  # phi read + b read + phi write per cell per HBM pass, fp64
 
 
 def parse():
@@ -339,7 +339,13 @@ def main():
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": ("k_sor_wf<%d> (%d red-black Poisson iterations per HBM pass)" % (fuse, fuse)
                                     if fuse > 1 else "k_sor<0> (one red-black Poisson iteration per HBM pass)"),
-                         "bytes_per_launch": BYTES_PER_POISSON_UPDATE * Np_local, "peak_source": peak_src},
+                         "bytes_per_launch": BYTES_PER_POISSON_UPDATE * Np_local, "peak_source": peak_src,
+                         # SURVEY 8(d) "effective algorithmic GB/s": the unfused pass's 24 B per cell per
+                         # iteration over the time per iteration (exceeds HBM when iterations are fused)
+                         "effective_per_iteration": {
+                             "bytes_per_cell": BYTES_PER_POISSON_UPDATE,
+                             "GBps": BYTES_PER_POISSON_UPDATE * Np_local / avg_iter_s / 1e9,
+                             "frac": BYTES_PER_POISSON_UPDATE * Np_local / avg_iter_s / 1e9 / peak}},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
         }
         print(json.dumps(line), flush=True)
