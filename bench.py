@@ -57,7 +57,7 @@ def parse():
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--cpu-sample-n", type=int, default=0, help="oracle sample grid (0 = auto)")
     ap.add_argument("--sor-fuse", type=int, default=0,
-                    help="Poisson iterations fused per HBM pass (0 = library default 3; slabs use 1)")
+                    help="Poisson iterations fused per HBM pass (0 = library default 3)")
     ap.add_argument("--sor-batch", type=int, default=0,
                     help="> 0: host-launched SOR iterations in batches of this size instead of the graph WHILE loop")
     return ap.parse_args()
@@ -270,7 +270,7 @@ def main():
     # Poisson loop on the launch stream / passes (it_p / m per step)
     Np_local = cfg.nx * (j1 - j0)
     it_p = float(stats[:, 2].sum())
-    fuse = 1 if world > 1 else (args.sor_fuse or 3)
+    fuse = args.sor_fuse or 3
     passes = float(sum(np.ceil(stats[:, 2] / fuse)))
     avg_iter_s = (psor_ms / 1e3) / max(it_p, 1.0)
     avg_launch_s = (psor_ms / 1e3) / max(passes, 1.0)

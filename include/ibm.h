@@ -89,7 +89,7 @@ typedef struct {
                                    ignored, get/set_fields cover the whole grid) */
     int sor_fuse;               /* Poisson red-black iterations fused per HBM pass (temporal
                                    blocking): 0 = default (3), 1 = one iteration
-                                   per pass, 2..4; slab-decomposed runs use 1 */
+                                   per pass, 2..4; slabs of fewer than 2m rows use 1 */
 } ibm_config;
 
 typedef struct {

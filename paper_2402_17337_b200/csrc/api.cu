@@ -325,7 +325,7 @@ bool make_maps(Slab &s, int wf_m) {
 // ---------------------------------------------------------------- halos and reductions
 // exchange 2 ghost rows of one family buffer (selected per slab by `pick`)
 template <class Pick>
-int halo(Ctx &c, Pick pick) {
+int halo(Ctx &c, Pick pick, int rows = 2) {
   const size_t esz = sizeof(double);
   if (c.loopback) {
     for (size_t r = 0; r + 1 < c.sl.size(); ++r) {
@@ -333,8 +333,8 @@ int halo(Ctx &c, Pick pick) {
       const Geo *glo, *gup;
       pick(c.sl[r], &lo, &glo);
       pick(c.sl[r + 1], &up, &gup);
-      const size_t bytes = (size_t)kGhost * glo->pitch * esz;
-      CK(cudaMemcpyAsync(up + gup->off(0, -kGhost), lo + glo->off(0, glo->nj - kGhost), bytes,
+      const size_t bytes = (size_t)rows * glo->pitch * esz;
+      CK(cudaMemcpyAsync(up + gup->off(0, -rows), lo + glo->off(0, glo->nj - rows), bytes,
                          cudaMemcpyDeviceToDevice, c.stream));
       CK(cudaMemcpyAsync(lo + glo->off(0, glo->nj), up + gup->off(0, 0), bytes, cudaMemcpyDeviceToDevice,
                          c.stream));
@@ -347,14 +347,14 @@ int halo(Ctx &c, Pick pick) {
   const Geo *g;
   pick(c.sl[0], &buf, &g);
   const int r = c.sl[0].rank;
-  const size_t cnt = (size_t)kGhost * g->pitch;
+  const size_t cnt = (size_t)rows * g->pitch;
   NK(ncclGroupStart());
   if (r > 0) {
     NK(ncclSend(buf + g->off(0, 0), cnt, ncclFloat64, r - 1, comm, c.stream));
-    NK(ncclRecv(buf + g->off(0, -kGhost), cnt, ncclFloat64, r - 1, comm, c.stream));
+    NK(ncclRecv(buf + g->off(0, -rows), cnt, ncclFloat64, r - 1, comm, c.stream));
   }
   if (r < c.nranks - 1) {
-    NK(ncclSend(buf + g->off(0, g->nj - kGhost), cnt, ncclFloat64, r + 1, comm, c.stream));
+    NK(ncclSend(buf + g->off(0, g->nj - rows), cnt, ncclFloat64, r + 1, comm, c.stream));
     NK(ncclRecv(buf + g->off(0, g->nj), cnt, ncclFloat64, r + 1, comm, c.stream));
   }
   NK(ncclGroupEnd());
@@ -365,6 +365,12 @@ int halo(Ctx &c, Pick pick) {
   do {                                                                        \
     int st_ = halo(c, [&](Slab &s, double **b, const Geo **g) { expr; });     \
     if (st_) return st_;                                                      \
+  } while (0)
+// the same with `rows` ghost rows (the fused Poisson pass needs 2m)
+#define HALO_ROWS(rows, expr)                                                   \
+  do {                                                                          \
+    int st_ = halo(c, [&](Slab &s, double **b, const Geo **g) { expr; }, rows); \
+    if (st_) return st_;                                                        \
   } while (0)
 
 bool multi(const Ctx &c) { return c.sl.size() > 1 || c.nranks > 1; }
@@ -488,13 +494,15 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
     *buf_out = (s0 + *k_out) & 1;
     return IBM_OK;
   }
-  // temporally blocked Poisson passes (single slab)
-  const bool wf = !helm && !mult && c.wf_m >= 2;
-  WfArgs wa;
-  if (wf) {
+  // temporally blocked Poisson passes (every slab; decomposed runs exchange 2m
+  // halo rows per pass and reduce the m residuals after it)
+  const bool wf = !helm && c.wf_m >= 2;
+  std::vector<WfArgs> was(wf ? c.sl.size() : 0);
+  for (size_t r = 0; r < was.size(); ++r) {
+    WfArgs &wa = was[r];
     std::memset(&wa, 0, sizeof(wa));
-    const Slab &s = c.sl[0];
-    const SorFam &f = args[0].f[0];
+    const Slab &s = c.sl[r];
+    const SorFam &f = args[r].f[0];
     wa.tmb = s.tm_wbp;
     wa.flag = f.flag; wa.g = f.g; wa.box = f.box;
     wa.cE = f.cE; wa.cW = f.cW; wa.cD = f.cD; wa.cN = f.cN; wa.cS = f.cS;
@@ -502,6 +510,7 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
     wa.omega = omega; wa.omc = 1.0 - omega; wa.tol = tol;
     wa.maxit = maxit; wa.check_every = cfg.check_every;
     wa.rho_bits = c.rho_bits; wa.ctl = c.ctl;
+    wa.multi = mult ? 1 : 0;
     wf_plan(wa, c.wf_m);
   }
   // one single-iteration pass of every slab (halos first when decomposed)
@@ -548,11 +557,23 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
     const int kend = std::min(maxit, k + batch - 1);
     while (k <= kend) {
       if (wf && k + c.wf_m - 1 <= maxit) {
-        wa.k = k;
-        wa.xout = c.sl[0].phi[cur ^ 1];
-        wa.tmx = c.sl[0].tm_wphi[cur];
-        CK(launch_sor_wf(wa, c.wf_m, c.stream));
-        ++c.launches;
+        const int in = cur;
+        if (mult) HALO_ROWS(2 * c.wf_m, (*b = s.phi[in], *g = &s.gp));
+        for (size_t r = 0; r < c.sl.size(); ++r) {
+          WfArgs &wa = was[r];
+          wa.k = k;
+          wa.xout = c.sl[r].phi[in ^ 1];
+          wa.tmx = c.sl[r].tm_wphi[in];
+          CK(launch_sor_wf(wa, c.wf_m, c.stream));
+          ++c.launches;
+        }
+        if (mult) {
+          if (!c.loopback)
+            NK(ncclAllReduce(c.rho_bits + k, c.rho_bits + k, c.wf_m, ncclUint64, ncclMax, (ncclComm_t)c.nccl,
+                             c.stream));
+          launch_sor_check(c.ctl, c.rho_bits, k, maxit, cfg.check_every, tol, c.stream, c.wf_m);
+          ++c.launches;
+        }
         passes.push_back({k, c.wf_m, cur});
         k += c.wf_m;
       } else {
@@ -648,7 +669,7 @@ int step_once(Ctx &c, ibm_step_stats *st) {
   CK(cudaEventRecord(c.ev[2], c.stream));
   // a5 masks -> q, Poisson rhs; phi := 0 on inactive cells
   for (Slab &s : c.sl) c.launches += launch_prhs(c, s, s.us[ures], s.vs[ures], s.phi[c.phi_cur]);
-  if (multi(c)) HALO((*b = s.bp, *g = &s.gp));
+  if (multi(c)) HALO_ROWS(c.wf_m >= 2 ? 2 * c.wf_m : 2, (*b = s.bp, *g = &s.gp));
   CK(cudaEventRecord(c.ev[3], c.stream));
   // a6 Poisson SOR, warm start
   int kp = 0;
@@ -763,8 +784,16 @@ int ibm_init(const ibm_config *cfg, void *d_workspace, size_t bytes, void *cuda_
   c.nccl = nullptr;
   c.hint_uv = 16;
   c.hint_p = 64;
-  // temporal blocking of the Poisson pass needs 2 m halo rows: single slab only
-  c.wf_m = (cfg->loopback || cfg->nranks > 1) ? 1 : (cfg->sor_fuse == 0 ? 3 : cfg->sor_fuse);
+  // Poisson iterations fused per pass.  A decomposed grid exchanges 2m rows per
+  // fused pass, so every slab must own that many; decided from cfg alone so that
+  // all ranks agree (their collectives must match).
+  c.wf_m = cfg->sor_fuse == 0 ? 3 : cfg->sor_fuse;
+  if (cfg->nranks > 1)
+    for (int r = 0; r < cfg->nranks; ++r) {
+      int j0 = 0, j1 = 0;
+      slab_rows(cfg->ny, cfg->nranks, r, &j0, &j1);
+      if (2 * c.wf_m > j1 - j0) c.wf_m = 1;
+    }
   if (c.loopback)
     for (int r = 0; r < cfg->nranks; ++r) c.sl.push_back(make_slab(*cfg, r));
   else

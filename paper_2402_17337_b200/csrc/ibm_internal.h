@@ -1,7 +1,7 @@
 // Internal declarations of the B200 library (not part of the C ABI).
 // Layout of every staggered family in HBM: row-major, x fastest,
-// row pitch a multiple of 32 doubles (256 B), 2 ghost rows below and above the
-// slab's owned rows (the halo of the fused red-black pass); out-of-range
+// row pitch a multiple of 32 doubles (256 B, padded off 4 KB multiples), kGhost
+// ghost rows below and above the slab's owned rows; out-of-range
 // columns are never stored -- kernels treat them as 0 with coefficient 0,
 // exactly like the oracle's out-of-range reads.
 #pragma once
@@ -17,7 +17,9 @@
 
 namespace ibm {
 
-constexpr int kGhost = 2;  // ghost rows per side
+// ghost rows per side: 2 for the one-iteration passes, 2m for a pass fusing m
+// red-black iterations on a decomposed grid (m <= 4)
+constexpr int kGhost = 8;
 enum Tag : uint8_t { FLUID = 0, SOLID = 1, FORCING = 2 };
 // Poisson cell flags; 0 = active cell with all four faces open (the default
 // outside the body envelope box).  Closed bits are only set on interior faces.
@@ -93,6 +95,7 @@ struct WfArgs {
   const double *cE, *cW, *cD, *cN, *cS;
   int ui0, ui1, uj0, uj1;
   int strips, segs, L, items;
+  int multi;            // several slabs / ranks: the decision runs after the residual reduction
   double omega, omc, tol;
   int k, maxit, check_every;
   unsigned long long *rho_bits;
@@ -172,7 +175,7 @@ int wf_box_cols();
 void wf_plan(WfArgs &a, int m);
 cudaError_t launch_sor_wf(const WfArgs &a, int m, cudaStream_t st);
 void launch_sor_check(SorCtl *ctl, const unsigned long long *rho_bits, int k, int maxit, int check_every,
-                      double tol, cudaStream_t st);
+                      double tol, cudaStream_t st, int m = 1);
 int launch_outlet_fill(const Ctx &c, const Slab &s, double *us, const double *vs);
 int launch_prhs(const Ctx &c, const Slab &s, const double *us, const double *vs, double *phi_start);
 int launch_correct(const Ctx &c, const Slab &s, const double *us, const double *vs, const double *phi);

@@ -75,11 +75,13 @@ __global__ void k_pflags(uint8_t *__restrict__ pf, const uint8_t *__restrict__ t
   int jl = box.j0 + blockIdx.y * blockDim.y + threadIdx.y;
   if (i >= box.i1 || jl >= box.j1) return;
   int gj = gp.gj0 + jl;
-  auto act0 = [&](int ii, int jj) -> bool { return tp[gp.off(ii, jj)] == FLUID; };
+  // rows beyond the stored ghost rows: treated as inactive (only the outermost
+  // ghost row's flags depend on them, and that row is never updated)
+  auto act0 = [&](int ii, int jj) -> bool { return jj >= -kGhost && jj < gp.nj + kGhost && tp[gp.off(ii, jj)] == FLUID; };
   bool a0 = act0(i, jl);
   bool oE = (i + 1 <= nx - 1) && tu[gu.off(i + 1, jl)] == FLUID && a0 && act0(i + 1, jl);
   bool oW = (i >= 1) && tu[gu.off(i, jl)] == FLUID && act0(i - 1, jl) && a0;
-  bool oN = (gj + 1 <= ny - 1) && tv[gv.off(i, jl + 1)] == FLUID && a0 && act0(i, jl + 1);
+  bool oN = (gj + 1 <= ny - 1) && jl + 1 < gv.nj + kGhost && tv[gv.off(i, jl + 1)] == FLUID && a0 && act0(i, jl + 1);
   bool oS = (gj >= 1) && tv[gv.off(i, jl)] == FLUID && act0(i, jl - 1) && a0;
   uint8_t f = 0;
   if (i + 1 <= nx - 1 && !oE) f |= PF_E;
@@ -479,10 +481,11 @@ int launch_classify(const Ctx &c, const Slab &s, double yb) {
 
 int launch_pflags(const Ctx &c, const Slab &s) {
   if (s.bpb.empty()) return 0;
-  // flags are needed on the owned rows and one ghost row each side
+  // flags are needed on the owned rows and on the ghost rows a decomposed pass
+  // updates: one for the one-iteration pass, 2m - 1 <= kGhost - 1 for a pass fusing m
   BBox box = s.bpb;
-  box.j0 = box.j0 < -1 ? -1 : box.j0;
-  box.j1 = box.j1 > s.gp.nj + 1 ? s.gp.nj + 1 : box.j1;
+  box.j0 = box.j0 < 1 - kGhost ? 1 - kGhost : box.j0;
+  box.j1 = box.j1 > s.gp.nj + kGhost - 1 ? s.gp.nj + kGhost - 1 : box.j1;
   if (box.empty()) return 0;
   dim3 blk(32, 8);
   k_pflags<<<grid2(box.i1 - box.i0, box.j1 - box.j0, blk), blk, 0, c.stream>>>(s.pf, s.tp, s.tu, s.tv, s.gp, s.gu,

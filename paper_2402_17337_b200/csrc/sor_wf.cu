@@ -380,6 +380,7 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
       for (int v = 0; v < WNW; ++v) mx = umax64(mx, wmax[v][i]);
       if (mx) atomicMax(&A.rho_bits[A.k + i], mx);
     }
+    if (A.multi) return;  // decided by k_sor_check after the cross-slab reduction
     __threadfence();
     const unsigned tk = atomicAdd(&A.ctl->ticket, 1u);
     if (tk == gridDim.x - 1) {

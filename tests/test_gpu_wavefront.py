@@ -102,3 +102,23 @@ def test_poisson_iterate_fused_vs_unfused(mods, wf_rows, m, iters):
         g.close()
     assert np.array_equal(out[0][0], out[1][0])
     assert out[0][1] == out[1][1] or (np.isnan(out[0][1]) and np.isnan(out[1][1]))
+
+
+@pytest.mark.parametrize("m", FUSE)
+@pytest.mark.parametrize("P", [2, 3])
+def test_loopback_slabs_fused(mods, wf_rows, m, P):
+    """Slab decomposition with the fused pass: 2m halo rows exchanged per pass, the
+    m residuals reduced after it -- bit-identical to the oracle."""
+    wf_rows(10)
+    cfg = I.cfg1(steps=3, maxit_p=700)
+    o, g, ro, rg = run_pair(mods, cfg, cfg.steps, nranks=P, loopback=True, sor_batch=5, sor_fuse=m)
+    assert_parity(o, g, ro, rg)
+
+
+@pytest.mark.parametrize("m", [3])
+def test_loopback_cylinder_fused(mods, wf_rows, m):
+    """Body crossing a slab boundary (cylinder centred on the domain's mid row)."""
+    wf_rows(0)
+    cfg = I.cfg2(nx=96, ny=72, steps=3, maxit_p=400)
+    o, g, ro, rg = run_pair(mods, cfg, cfg.steps, nranks=2, loopback=True, sor_fuse=m)
+    assert_parity(o, g, ro, rg)
