@@ -296,8 +296,9 @@ typedef struct {
 /* Runs red-black SOR on nsys independent systems jointly: one iteration = red
  * sweep of every system, then black sweep of every system; rho_k = max over all
  * updates of |gs - x_old|.  Node update (R2, R13):
- *   n = fma(aN, xN, fma(aE, xE, fma(aW, xW, fma(aS, xS, b))));  gs = n * (1/aP);
- *   d = gs - x_old;  x = fma(omega, d, x_old) (= (1-omega) x_old + omega gs);  e = |d|.
+ *   n = fma(aN, xN, fma(aE, xE, fma(aW, xW, fma(aS, xS, b))));  r = 1/aP;
+ *   d = fma(n, r, -x_old) (= gs - x_old, gs = n/aP, one rounding);
+ *   x = fma(omega, d, x_old) (= (1-omega) x_old + omega gs);  e = |d|.
  *   fma is C99 fma (one rounding); 1/aP is the correctly rounded reciprocal (one
  *   IEEE division) -- reading R13.  Colour red = (i+j) even.  Returns iterations; status
  * ORC_ERR_DIVERGED if rho is NaN, ORC_WARN_NOCONV if maxit reached above tol. */
@@ -326,9 +327,8 @@ static int sor_run(int nsys, sor_sys *sys, double omega, double tol, int maxit,
                         double num = fma(S->aN[id], xN, fma(S->aE[id], xE, fma(S->aW[id], xW,
                                          fma(S->aS[id], xS, S->b[id]))));
                         double rcp = 1.0 / S->aP[id];
-                        double gs = num * rcp;
                         double xo = S->x[id];
-                        double d = gs - xo;
+                        double d = fma(num, rcp, -xo); /* gs - x_old, gs = num * rcp (R13) */
                         double e = fabs(d);
                         S->x[id] = fma(omega, d, xo);
                         if (isnan(e) || isnan(rho)) rho = NAN;

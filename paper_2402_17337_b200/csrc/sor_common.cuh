@@ -11,6 +11,15 @@ namespace ibm {
 __device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) {
   return a > b ? a : b;
 }
+// |d| as its IEEE bit pattern (order-preserving for |d| >= 0; NaN sorts above
+// every number).  The sign bit is cleared with an integer AND on the high word:
+// written as a plain 64-bit AND, ptxas turns it into DADD |d| on the fp64 pipe.
+__device__ __forceinline__ unsigned long long abs_bits(double d) {
+  unsigned lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "d"(d));
+  asm("and.b32 %0, %0, 0x7fffffff;" : "+r"(hi));
+  return ((unsigned long long)hi << 32) | lo;
+}
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long *bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");

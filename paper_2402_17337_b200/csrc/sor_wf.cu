@@ -127,11 +127,11 @@ __device__ __forceinline__ void wf_fast(double2 (&X)[NS][W], const double2 (&B)[
     const double xo = rd(X[st][Q], E), xN = rd(X[st][QN], E), xS = rd(X[st][QS], E);
     const double nm =
         __fma_rn(aN, xN, __fma_rn(C.aE[st][E], xE, __fma_rn(C.aW[st][E], xW, __fma_rn(aS, xS, rd(B[st][Q], E)))));
-    const double d = nm * C.yu[st][E] - xo;  // gs - x_old (--fmad=false: two roundings)
+    const double d = __fma_rn(nm, C.yu[st][E], -xo);  // gs - x_old, one rounding (R13)
     const double xn = __fma_rn(omega, d, xo);
     wr(X[st][Q], E, (!EDGE || C.in[st][E]) ? xn : xo);
     // |gs - xo| as a bit pattern: clearing the sign bit is fabs (integer pipe)
-    const unsigned long long e = (unsigned long long)__double_as_longlong(d) & 0x7fffffffffffffffull;
+    const unsigned long long e = abs_bits(d);
     tmax[st] = ((!EDGE || C.in[st][E]) && own && e > tmax[st]) ? e : tmax[st];
   }
 }
@@ -173,10 +173,10 @@ __device__ __forceinline__ void wf_slow(double2 (&X)[NS][W], const double2 (&B)[
     const double xW = E ? X[st][Q].x : nb[st];
     const double xo = rd(X[st][Q], E), xN = rd(X[st][QN], E), xS = rd(X[st][QS], E);
     const double nm = __fma_rn(aN, xN, __fma_rn(aE, xE, __fma_rn(aW, xW, __fma_rn(aS, xS, rd(B[st][Q], E)))));
-    const double d = nm * __drcp_rn(aP) - xo;
+    const double d = __fma_rn(nm, __drcp_rn(aP), -xo);
     if (u) {
       wr(X[st][Q], E, __fma_rn(omega, d, xo));
-      if (own) tmax[st] = umax64(tmax[st], (unsigned long long)__double_as_longlong(d) & 0x7fffffffffffffffull);
+      if (own) tmax[st] = umax64(tmax[st], abs_bits(d));
     }
   }
 }
@@ -321,11 +321,16 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
     // Irregular rows of the item (outside the family, in the body box, or with
     // row coefficients other than the reference): the chunks whose rows
     // rb-2WM .. rb+W-2 meet [irr0, irr1] take the predicated path.
+    // (unconditional loads of clamped rows, unrolled: the loads of several rows
+    // are in flight together instead of one dependent L2 round trip per test)
     int irr0 = INT_MAX, irr1 = INT_MIN;
+#pragma unroll 4
     for (int r = rs - 2 * WM + l; r <= rs + nch * W - 2; r += 32) {
       const int gj = g.gj0 + r;
-      const bool reg = gj >= A.uj0 && gj < A.uj1 && !(boxstrip && r >= A.box.j0 && r < A.box.j1) &&
-                       A.cN[gj] == cN0 && A.cS[gj] == cS0;
+      const int gjc = min(max(gj, 0), g.NJ - 1);
+      const double cn = __ldg(A.cN + gjc), cs = __ldg(A.cS + gjc);
+      const bool reg = (gj >= A.uj0) & (gj < A.uj1) & !(boxstrip & (r >= A.box.j0) & (r < A.box.j1)) &
+                       (cn == cN0) & (cs == cS0);
       if (!reg) {
         irr0 = min(irr0, r);
         irr1 = max(irr1, r);
