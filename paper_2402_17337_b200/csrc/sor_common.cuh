@@ -20,6 +20,16 @@ __device__ __forceinline__ unsigned long long abs_bits(double d) {
   asm("and.b32 %0, %0, 0x7fffffff;" : "+r"(hi));
   return ((unsigned long long)hi << 32) | lo;
 }
+// abs_bits(d) & (m:m): the whole pattern is zeroed where the mask m is 0 (a term
+// that is not counted), folded into the sign-clearing AND
+__device__ __forceinline__ unsigned long long abs_bits_masked(double d, unsigned m) {
+  unsigned lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "d"(d));
+  asm("and.b32 %0, %0, 0x7fffffff;" : "+r"(hi));
+  hi &= m;
+  lo &= m;
+  return ((unsigned long long)hi << 32) | lo;
+}
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long *bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");

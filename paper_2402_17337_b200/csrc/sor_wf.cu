@@ -39,19 +39,22 @@ namespace ibm {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
+// One warp per CTA (measured, 8192^2 m = 3: 0.134 ms/iteration against 0.145 with
+// 4 warps per CTA): a CTA's resources are released as soon as its one item is
+// done, so slow items (body, edges) do not hold fast ones at the CTA barrier.
 #ifndef WF_NW
-#define WF_NW 4
+#define WF_NW 1
 #endif
 constexpr int WNW = WF_NW;  // warps per CTA (independent work items)
 constexpr int WNT = 32 * WNW;
-// stages per warp: 2 for m = 2, 3 for m >= 3 (measured: the deeper pass needs the
-// longer TMA lead; the shallower one loses a resident CTA with a third stage)
+// TMA stages per warp (double buffering: with 8 resident warps per SM one chunk
+// of lead keeps ~64 KB per SM in flight, measured as fast as three stages)
 template <int WM>
 __host__ __device__ constexpr int wf_nstg() {
 #ifdef WF_NSTG
   return WF_NSTG;
 #else
-  return WM >= 3 ? 3 : 2;
+  return 2;
 #endif
 }
 #ifndef WF_NS
@@ -70,7 +73,7 @@ constexpr size_t wf_smem() {
   return (size_t)WNW * wf_nstg<WM>() * (sizeof(WfStage<WM>) + sizeof(unsigned long long));
 }
 #ifndef WF_MINB
-#define WF_MINB 3
+#define WF_MINB (8 / WF_NW)  // 8 resident warps per SM (255 registers per thread)
 #endif
 // resident CTAs per SM the register budget is sized for (shared memory permitting)
 template <int WM>
@@ -81,7 +84,7 @@ constexpr int wf_min_blocks() {
 // Per-lane column data of the columns gi = i0 + 2 (l + 32 st) + e.
 struct WfCols {
   double aE[NS][2], aW[NS][2], sEW[NS][2], cD[NS][2], yu[NS][2];
-  bool in[NS][2];  // column inside the family's updatable range
+  unsigned inm[NS][2];  // all ones if the column is inside the family's updatable range, else 0
 };
 
 // Horizontal neighbour outside the pair for element E of window slot Q of every
@@ -113,9 +116,12 @@ __device__ __forceinline__ void wf_nb(const double2 (&X)[NS][W], double (&nb)[NS
 // One node update of the check-free path per pair set: element E of window
 // slot Q.  EDGE: the strip reaches past the family's columns; cells outside keep
 // their value and are not counted.
+// okm: all ones if the row is owned by the item, else 0 (an integer mask, not a
+// predicate: ptxas schedules the runtime-ownership chunks as tightly as the
+// all-owned ones then).
 template <int W, int Q, int E, bool EDGE>
 __device__ __forceinline__ void wf_fast(double2 (&X)[NS][W], const double2 (&B)[NS][W], const WfCols &C, double aN,
-                                        double aS, double omega, double omc, bool own,
+                                        double aS, double omega, double omc, unsigned okm,
                                         unsigned long long (&tmax)[NS]) {
   constexpr int QN = (Q + 1) % W, QS = (Q + W - 1) % W;
   double nb[NS];
@@ -129,10 +135,10 @@ __device__ __forceinline__ void wf_fast(double2 (&X)[NS][W], const double2 (&B)[
         __fma_rn(aN, xN, __fma_rn(C.aE[st][E], xE, __fma_rn(C.aW[st][E], xW, __fma_rn(aS, xS, rd(B[st][Q], E)))));
     const double d = __fma_rn(nm, C.yu[st][E], -xo);  // gs - x_old, one rounding (R13)
     const double xn = __fma_rn(omega, d, xo);
-    wr(X[st][Q], E, (!EDGE || C.in[st][E]) ? xn : xo);
-    // |gs - xo| as a bit pattern: clearing the sign bit is fabs (integer pipe)
-    const unsigned long long e = abs_bits(d);
-    tmax[st] = ((!EDGE || C.in[st][E]) && own && e > tmax[st]) ? e : tmax[st];
+    wr(X[st][Q], E, (!EDGE || C.inm[st][E]) ? xn : xo);
+    // |gs - xo| as a bit pattern (sign cleared on the integer pipe), 0 where not counted
+    const unsigned long long e = abs_bits_masked(d, EDGE ? (okm & C.inm[st][E]) : okm);
+    tmax[st] = e > tmax[st] ? e : tmax[st];
   }
 }
 
@@ -210,6 +216,9 @@ __device__ __forceinline__ void sfor(F &&f) {
 // chunk touches is owned by the item (the residual needs no row test; halo
 // lanes are dropped once per item).  rb is even and W is even, so the slot and
 // the colour element of every half-sweep are compile-time constants.
+// (Compile-time ownership classes for the first / last two chunks of a segment
+// were measured 14 % slower overall: the extra rarely-run chunk bodies miss in
+// the instruction cache.)
 template <int WM, int TP, int MODE, bool OWN>
 __device__ __forceinline__ void wf_chunk(double2 (&X)[NS][2 * WM + 2], double2 (&B)[NS][2 * WM + 2],
                                          const WfStage<WM> &S, const WfCols &C, const WfArgs &A, int rb, int j0,
@@ -233,9 +242,15 @@ __device__ __forceinline__ void wf_chunk(double2 (&X)[NS][2 * WM + 2], double2 (
       constexpr int Q = ((q - 1 - h) % W + W) % W;  // slot of row rb + q - 1 - h
       constexpr int E = (TP + Q + h) & 1;           // red (h even): (i + j) even
       const int r = rb + q - 1 - h;
-      const bool own = OWN ? true : (r >= j0 && r < j1);
+      [[maybe_unused]] const bool own = OWN || (r >= j0 && r < j1);
+      // owned-row mask from the sign bits of r - j0 and j1 - 1 - r (no predicate)
+      unsigned okm = 0xffffffffu;
+      if (!OWN)  // (opaque to the compiler, which would otherwise turn it back into selects)
+        asm("{\n .reg .b32 t;\n or.b32 t, %1, %2;\n shr.s32 t, t, 31;\n not.b32 %0, t;\n}"
+            : "=r"(okm)
+            : "r"(r - j0), "r"(j1 - 1 - r));
       if constexpr (MODE > 0)
-        wf_fast<W, Q, E, MODE == 1>(X, B, C, cN0, cS0, omega, omc, own, tmax[h / 2]);
+        wf_fast<W, Q, E, MODE == 1>(X, B, C, cN0, cS0, omega, omc, okm, tmax[h / 2]);
       else
         wf_slow<W, Q, E>(X, B, C, A, r, i0, hasf, omega, omc, own, tmax[h / 2]);
     });
@@ -311,7 +326,7 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
         C.aW[s][e] = cW;
         C.sEW[s][e] = cE + cW;
         C.yu[s][e] = __drcp_rn((C.sEW[s][e] + (cN0 + cS0)) + C.cD[s][e]);
-        C.in[s][e] = gi >= A.ui0 && gi < A.ui1;
+        C.inm[s][e] = (gi >= A.ui0 && gi < A.ui1) ? 0xffffffffu : 0u;
       }
     double2 X[NS][W], B[NS][W];
 #pragma unroll
@@ -355,7 +370,9 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
         wf_chunk<WM, TP, 0, false>(X, B, st[s], C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax);
       __syncwarp();
       if (l == 0 && c + NSTG < nch) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        // (no proxy fence: the stage's generic reads were all consumed by this
+        // warp's arithmetic before the __syncwarp above, so the TMA write cannot
+        // overtake them; a fence here is a MEMBAR that also drains the stores)
         mbar_expect_tx(&bar[s], kBytes);
         tma_load_2d(&st[s].x[0][0], &A.tmx, i0, rs + (c + NSTG) * W + kGhost, &bar[s]);
         tma_load_2d(&st[s].b[0][0], &A.tmb, i0, rs + (c + NSTG) * W + kGhost, &bar[s]);
@@ -438,16 +455,18 @@ cudaError_t wf_launch(const WfArgs &a, cudaStream_t s) {
 int wf_box_rows(int m) { return 2 * m + 2; }
 int wf_box_cols() { return SC; }
 
-// Strip / segment plan: segments of L owned rows, L = 64 for m = 2 and 128 for
-// m >= 3 (measured on 8192^2 over 48..512: short segments balance the slower
-// body / edge items over the waves, but every segment recomputes 4m halo rows
-// and rounds its 2m+2-row chunks up, which costs more for deeper fusion;
-// scripts/gpu_wf_tune.sh).  IBM_WF_ROWS overrides L for tuning; it is rounded up
+// Strip / segment plan: segments of L owned rows, L = 64 for m = 2 and 256 for
+// m >= 3 (measured on 8192^2, one warp per CTA, over 64..512: short segments
+// balance the slower body / edge items over the waves, but every segment
+// recomputes 4m halo rows and rounds its 2m+2-row chunks up, which costs more
+// for deeper fusion; m = 3: 64 0.139, 128 0.134, 192 0.166, 240 0.143, 256 0.132,
+// 512 0.142 ms/iteration -- not monotone, so re-measure for other grids;
+// scripts/gpu_wf_rows.sh).  IBM_WF_ROWS overrides L for tuning; it is rounded up
 // to even so colours stay compile-time.
 void wf_plan(WfArgs &a, int m) {
   const int ow = SC - 4 * m;
   a.strips = (a.g.ni + ow - 1) / ow;
-  int L = m == 2 ? 64 : 128;
+  int L = m == 2 ? 64 : 256;
   if (const char *e = std::getenv("IBM_WF_ROWS")) {
     const int v = std::atoi(e);
     if (v > 0) L = v;
