@@ -139,6 +139,50 @@ def cfg2(nx=512, ny=384, steps=2000, **kw) -> Config:
                   steps=steps, perturb=0.0, **kw)
 
 
+# Production mesh levels of the paper's input-scaling study (Table 2
+# P:175-186): M1/M2/M3 = 6/12/18 lakh cells.  The paper gives the domain
+# and Delta x = Delta y = 0.004 but not the uniform patch or stretch ratio
+# (S:80-81 open question): reading R28 -- uniform patch x in [-1, 2] (chord plus
+# near wake), y in [-0.75, 0.75] (plunge envelope +-(h + b) plus a 0.5c margin),
+# geometric ratio 1.05 outside, h_min chosen per level so that nx*ny hits
+# the level's cell count within 1 %.  M1 comes out at h_min ~ 0.004.
+MESH_LEVEL_CELLS = {1: 600_000, 2: 1_200_000, 3: 1_800_000}
+PAPER_UNIFORM_PATCH = (-1.0, 2.0, -0.75, 0.75)
+
+
+def production_axes(cells: int, ratio: float = 1.05):
+    """(xn, yn, h_min) of the stretched paper-domain grid with nx*ny within 1 %
+    of `cells`.  h_min = 3/n with n even, so both uniform patches (3 and 1.5
+    chords) hold a whole number of cells; the count is monotone in n."""
+    x0, x1, y0, y1 = PAPER_DOMAIN
+    ux0, ux1, uy0, uy1 = PAPER_UNIFORM_PATCH
+    best = None
+    for n in range(100, 4000, 2):
+        h = (ux1 - ux0) / n
+        xn = stretched_axis(x0, x1, ux0, ux1, h, ratio)
+        yn = stretched_axis(y0, y1, uy0, uy1, h, ratio)
+        cnt = (len(xn) - 1) * (len(yn) - 1)
+        if best is None or abs(cnt - cells) < abs(best[3] - cells):
+            best = (xn, yn, h, cnt)
+        if cnt > cells:
+            break
+    if abs(best[3] - cells) > 0.01 * cells:
+        raise ValueError("production_axes: no grid within 1 %% of %d cells" % cells)
+    return best[0], best[1], best[2]
+
+
+def cfg3(level=1, steps=1000, **kw) -> Config:
+    """BJ configs[2]: plunging foil, Re = 500, k = 2 pi, h = 0.16 on the
+    paper's stretched production mesh M1/M2/M3 (reading R28), dt = 1e-4
+    (P:59), impulsive start; timing over the first 1000 steps (Table 2)."""
+    xn, yn, h = production_axes(MESH_LEVEL_CELLS[level])
+    c = Config("cfg3-foil-M%d-%dx%d" % (level, len(xn) - 1, len(yn) - 1), xn, yn, Re=PAPER_RE,
+               dt=kw.pop("dt", PAPER_DT), body=Body(), steps=steps, **kw)
+    c.extra["h_min"] = h
+    c.extra["level"] = level
+    return c
+
+
 def cfg4(n=8192, steps=3, **kw) -> Config:
     """BJ configs[3]: N x N uniform grid on the paper domain, foil as the
     paper's validation case, impulsive start, tol_p = 1e-6."""

@@ -787,13 +787,15 @@ int ibm_init(const ibm_config *cfg, void *d_workspace, size_t bytes, void *cuda_
   // Poisson iterations fused per pass.  A decomposed grid exchanges 2m rows per
   // fused pass, so every slab must own that many; decided from cfg alone so that
   // all ranks agree (their collectives must match).
+  // Automatic choice (sor_fuse = 0): m = 3 where the grid gives the fused pass
+  // enough work items, else the one-iteration pass (wf_viable).
   c.wf_m = cfg->sor_fuse == 0 ? 3 : cfg->sor_fuse;
-  if (cfg->nranks > 1)
-    for (int r = 0; r < cfg->nranks; ++r) {
-      int j0 = 0, j1 = 0;
-      slab_rows(cfg->ny, cfg->nranks, r, &j0, &j1);
-      if (2 * c.wf_m > j1 - j0) c.wf_m = 1;
-    }
+  for (int r = 0; r < cfg->nranks; ++r) {
+    int j0 = 0, j1 = cfg->ny;
+    if (cfg->nranks > 1) slab_rows(cfg->ny, cfg->nranks, r, &j0, &j1);
+    if (2 * c.wf_m > j1 - j0) c.wf_m = 1;
+    if (cfg->sor_fuse == 0 && c.wf_m >= 2 && !wf_viable(cfg->nx, j1 - j0, c.wf_m)) c.wf_m = 1;
+  }
   if (c.loopback)
     for (int r = 0; r < cfg->nranks; ++r) c.sl.push_back(make_slab(*cfg, r));
   else

@@ -173,6 +173,7 @@ void launch_sor_iteration(const SorArgs &a, cudaStream_t st, int grid);
 int wf_box_rows(int m);
 int wf_box_cols();
 void wf_plan(WfArgs &a, int m);
+bool wf_viable(int ni, int nj, int m);
 cudaError_t launch_sor_wf(const WfArgs &a, int m, cudaStream_t st);
 void launch_sor_check(SorCtl *ctl, const unsigned long long *rho_bits, int k, int maxit, int check_every,
                       double tol, cudaStream_t st, int m = 1);

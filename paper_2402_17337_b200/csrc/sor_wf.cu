@@ -456,17 +456,43 @@ int wf_box_rows(int m) { return 2 * m + 2; }
 int wf_box_cols() { return SC; }
 
 // Strip / segment plan: segments of L owned rows, L = 64 for m = 2 and 256 for
-// m >= 3 (measured on 8192^2, one warp per CTA, over 64..512: short segments
+// m >= 3, halved (down to 32 / 64) while the items would not fill two waves
+// (measured on 8192^2, one warp per CTA, over 64..512: short segments
 // balance the slower body / edge items over the waves, but every segment
 // recomputes 4m halo rows and rounds its 2m+2-row chunks up, which costs more
 // for deeper fusion; m = 3: 64 0.139, 128 0.134, 192 0.166, 240 0.143, 256 0.132,
 // 512 0.142 ms/iteration -- not monotone, so re-measure for other grids;
 // scripts/gpu_wf_rows.sh).  IBM_WF_ROWS overrides L for tuning; it is rounded up
 // to even so colours stay compile-time.
+namespace {
+int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms < 1) sms = 1;
+  }
+  return sms;
+}
+// two waves of the 8 resident warps per SM
+int wf_items_target() { return 2 * 8 * sm_count(); }
+int wf_rows_default(int m) { return m == 2 ? 64 : 256; }
+int wf_rows_min(int m) { return m == 2 ? 32 : 64; }
+int wf_strips(int ni, int m) { return (ni + SC - 4 * m - 1) / (SC - 4 * m); }
+}  // namespace
+
+// The fused pass needs enough work items to fill the GPU at its shortest
+// segments; below that (mid-size grids, e.g. the 6-18 lakh production meshes)
+// the one-iteration pass with its 60 x 16 tiles is used instead.
+bool wf_viable(int ni, int nj, int m) {
+  return (long)wf_strips(ni, m) * ((nj + wf_rows_min(m) - 1) / wf_rows_min(m)) >= wf_items_target();
+}
+
 void wf_plan(WfArgs &a, int m) {
-  const int ow = SC - 4 * m;
-  a.strips = (a.g.ni + ow - 1) / ow;
-  int L = m == 2 ? 64 : 256;
+  a.strips = wf_strips(a.g.ni, m);
+  int L = wf_rows_default(m);
+  while (L > wf_rows_min(m) && (long)a.strips * ((a.g.nj + L - 1) / L) < wf_items_target()) L /= 2;
   if (const char *e = std::getenv("IBM_WF_ROWS")) {
     const int v = std::atoi(e);
     if (v > 0) L = v;

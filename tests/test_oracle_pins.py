@@ -535,3 +535,29 @@ def test_temporal_order_second(oracle_mod):
         e = [np.abs(res[i][k] - res[i + 1][k]).max() for i in range(3)]
         for i in range(2):
             assert 3.2 <= e[i] / e[i + 1] <= 4.8, (k, e)
+
+
+def test_production_mesh_presets():
+    """cfg3 mesh levels (reading R28): nx*ny within 1 % of 6/12/18 lakh,
+    axes span the paper domain exactly, uniform patch at h_min with a
+    whole number of cells, geometric ratio 1.05 outside except the
+    clamped last cell, M1 at h_min ~ 0.004."""
+    x0, x1, y0, y1 = I.PAPER_DOMAIN
+    for level, cells in I.MESH_LEVEL_CELLS.items():
+        c = I.cfg3(level=level)
+        assert abs(c.nx * c.ny - cells) <= 0.01 * cells
+        h = c.extra["h_min"]
+        for ax, lo, hi, ulo, uhi in ((c.xn, x0, x1, -1.0, 2.0), (c.yn, y0, y1, -0.75, 0.75)):
+            assert ax[0] == lo and ax[-1] == hi
+            d = np.diff(ax)
+            assert np.all(d > 0)
+            core = (ax[:-1] >= ulo - 1e-12) & (ax[1:] <= uhi + 1e-12)
+            assert np.allclose(d[core], h, rtol=1e-9, atol=0)
+            iu = np.nonzero(core)[0]
+            right = d[iu[-1] + 1:-1]          # stretched cells, clamped last one excluded
+            left = d[1:iu[0]][::-1]
+            for side in (right, left):
+                r = side[1:] / side[:-1]
+                assert np.allclose(r, 1.05, rtol=1e-9)
+                assert abs(side[0] / h - 1.05) < 1e-9
+    assert abs(I.cfg3(level=1).extra["h_min"] - 0.004) < 0.0005
