@@ -587,6 +587,32 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(&c.h_ctl[0], c.ctl, sizeof(SorCtl), cudaMemcpyDeviceToHost, c.stream));
     CK(cudaStreamSynchronize(c.stream));
+    if (c.h_ctl[0].k_done >= 0 && c.h_ctl[0].status == 4) {
+      // Provisional stop in a fused pass with the approximate (high-word) residual:
+      // replay that pass from its intact input with exact one-iteration passes --
+      // the same iterates, exact residuals, exact device-side decision.
+      const int kp = c.h_ctl[0].k_done;
+      size_t pi = 0;
+      while (pi < passes.size() && !(kp >= passes[pi].k0 && kp < passes[pi].k0 + passes[pi].m)) ++pi;
+      if (pi == passes.size()) { c.err = "provisional SOR stop at an iteration no pass covers"; return IBM_ERR_STATE; }
+      const Pass P = passes[pi];
+      passes.resize(pi);
+      std::memset(&c.h_ctl[1], 0, sizeof(SorCtl));
+      c.h_ctl[1].k_done = -1;
+      CK(cudaMemcpyAsync(c.ctl, &c.h_ctl[1], sizeof(SorCtl), cudaMemcpyHostToDevice, c.stream));
+      int in = P.in;
+      for (int kk = P.k0; kk < P.k0 + P.m; ++kk, in ^= 1) {
+        int r = single(kk, in, false);
+        if (r) return r;
+        passes.push_back({kk, 1, in});
+      }
+      k = P.k0 + P.m;
+      cur = in;
+      CK(cudaMemcpyAsync(&c.h_ctl[0], c.ctl, sizeof(SorCtl), cudaMemcpyDeviceToHost, c.stream));
+      CK(cudaStreamSynchronize(c.stream));
+      if (c.h_ctl[0].k_done >= 0) break;  // exact stop inside the replayed pass
+      continue;                            // the bound was not tight: carry on after the pass
+    }
     if (c.h_ctl[0].k_done >= 0) break;
     if (cfg.sor_batch <= 0) batch = std::min(2 * batch, 1024);
   }

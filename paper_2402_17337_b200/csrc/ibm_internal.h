@@ -63,7 +63,7 @@ struct SorFam {
 struct SorCtl {  // per-solve device control block
   unsigned long long rho_final;  // bits of rho at k_done
   int k_done;                    // -1 until converged / stopped
-  int status;                    // 0 converged, 1 maxit, 3 NaN
+  int status;                    // 0 converged, 1 maxit, 3 NaN, 4 provisional (k_sor_wf lower bound; host confirms)
   unsigned ticket;               // last-block counter
   int pad;
   unsigned long long rho3[3];    // persistent (cooperative) solve: residual of iteration k in slot k % 3

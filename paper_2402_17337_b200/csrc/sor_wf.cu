@@ -116,10 +116,28 @@ __device__ __forceinline__ void wf_nb(const double2 (&X)[NS][W], double (&nb)[NS
 // One node update of the check-free path per pair set: element E of window
 // slot Q.  EDGE: the strip reaches past the family's columns; cells outside keep
 // their value and are not counted.
+// Residual accumulation.  Exact (APX = false): max of the 64-bit pattern of |d|
+// (LOP3 + 2 ISETP + 2 SEL per node).  Approximate (APX = true): max of the high
+// 32 bits only (LOP3 + VIMNMX, which ptxas fuses pairwise into VIMNMX3); the pass
+// then reports a lower bound LB = H << 32 <= rho, so a stop is only provisional
+// and the host replays that pass with the exact one-iteration kernel (sor_solve).
+template <bool APX>
+__device__ __forceinline__ void wf_acc(unsigned long long &t, double d, unsigned m) {
+  if (APX) {
+    unsigned lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "d"(d));
+    hi &= 0x7fffffffu & m;
+    t = (unsigned long long)max((unsigned)t, hi);
+  } else {
+    const unsigned long long e = abs_bits_masked(d, m);
+    t = e > t ? e : t;
+  }
+}
+
 // okm: all ones if the row is owned by the item, else 0 (an integer mask, not a
 // predicate: ptxas schedules the runtime-ownership chunks as tightly as the
 // all-owned ones then).
-template <int W, int Q, int E, bool EDGE>
+template <int W, int Q, int E, bool EDGE, bool APX>
 __device__ __forceinline__ void wf_fast(double2 (&X)[NS][W], const double2 (&B)[NS][W], const WfCols &C, double aN,
                                         double aS, double omega, double omc, unsigned okm,
                                         unsigned long long (&tmax)[NS]) {
@@ -137,14 +155,13 @@ __device__ __forceinline__ void wf_fast(double2 (&X)[NS][W], const double2 (&B)[
     const double xn = __fma_rn(omega, d, xo);
     wr(X[st][Q], E, (!EDGE || C.inm[st][E]) ? xn : xo);
     // |gs - xo| as a bit pattern (sign cleared on the integer pipe), 0 where not counted
-    const unsigned long long e = abs_bits_masked(d, EDGE ? (okm & C.inm[st][E]) : okm);
-    tmax[st] = e > tmax[st] ? e : tmax[st];
+    wf_acc<APX>(tmax[st], d, EDGE ? (okm & C.inm[st][E]) : okm);
   }
 }
 
 // One node update of the predicated path (domain edges, body flags, arbitrary
 // row coefficients): the same per-cell logic as sor.cu's boundary tiles.
-template <int W, int Q, int E>
+template <int W, int Q, int E, bool APX>
 __device__ __forceinline__ void wf_slow(double2 (&X)[NS][W], const double2 (&B)[NS][W], const WfCols &C,
                                         const WfArgs &A, int r, int i0, bool hasf, double omega, double omc, bool own,
                                         unsigned long long (&tmax)[NS]) {
@@ -182,7 +199,7 @@ __device__ __forceinline__ void wf_slow(double2 (&X)[NS][W], const double2 (&B)[
     const double d = __fma_rn(nm, __drcp_rn(aP), -xo);
     if (u) {
       wr(X[st][Q], E, __fma_rn(omega, d, xo));
-      if (own) tmax[st] = umax64(tmax[st], abs_bits(d));
+      if (own) wf_acc<APX>(tmax[st], d, 0xffffffffu);
     }
   }
 }
@@ -219,7 +236,7 @@ __device__ __forceinline__ void sfor(F &&f) {
 // (Compile-time ownership classes for the first / last two chunks of a segment
 // were measured 14 % slower overall: the extra rarely-run chunk bodies miss in
 // the instruction cache.)
-template <int WM, int TP, int MODE, bool OWN>
+template <int WM, int TP, int MODE, bool OWN, bool APX>
 __device__ __forceinline__ void wf_chunk(double2 (&X)[NS][2 * WM + 2], double2 (&B)[NS][2 * WM + 2],
                                          const WfStage<WM> &S, const WfCols &C, const WfArgs &A, int rb, int j0,
                                          int j1, int i0, const bool (&lane_own)[NS], bool hasf, double cN0,
@@ -250,9 +267,9 @@ __device__ __forceinline__ void wf_chunk(double2 (&X)[NS][2 * WM + 2], double2 (
             : "=r"(okm)
             : "r"(r - j0), "r"(j1 - 1 - r));
       if constexpr (MODE > 0)
-        wf_fast<W, Q, E, MODE == 1>(X, B, C, cN0, cS0, omega, omc, okm, tmax[h / 2]);
+        wf_fast<W, Q, E, MODE == 1, APX>(X, B, C, cN0, cS0, omega, omc, okm, tmax[h / 2]);
       else
-        wf_slow<W, Q, E>(X, B, C, A, r, i0, hasf, omega, omc, own, tmax[h / 2]);
+        wf_slow<W, Q, E, APX>(X, B, C, A, r, i0, hasf, omega, omc, own, tmax[h / 2]);
     });
     // row rb + q - 2WM has received its last half-sweep: store the owned columns
     const int ro = rb + q - 2 * WM;
@@ -267,7 +284,7 @@ __device__ __forceinline__ void wf_chunk(double2 (&X)[NS][2 * WM + 2], double2 (
   });
 }
 
-template <int WM, int TP>
+template <int WM, int TP, bool APX>
 __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __grid_constant__ WfArgs A) {
   constexpr int W = 2 * WM + 2, OW = SC - 4 * WM, NSTG = wf_nstg<WM>();
   constexpr unsigned kBytes = 2u * W * SC * 8;
@@ -361,13 +378,13 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
       mbar_wait_warp(&bar[s], (c / NSTG) & 1);
       const bool ownall = rb - 2 * WM >= j0 && rb + W - 2 < j1;
       if (fast && interior && ownall)
-        wf_chunk<WM, TP, 2, true>(X, B, st[s], C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax);
+        wf_chunk<WM, TP, 2, true, APX>(X, B, st[s], C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax);
       else if (fast && interior)
-        wf_chunk<WM, TP, 2, false>(X, B, st[s], C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax);
+        wf_chunk<WM, TP, 2, false, APX>(X, B, st[s], C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax);
       else if (fast)
-        wf_chunk<WM, TP, 1, false>(X, B, st[s], C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax);
+        wf_chunk<WM, TP, 1, false, APX>(X, B, st[s], C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax);
       else
-        wf_chunk<WM, TP, 0, false>(X, B, st[s], C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax);
+        wf_chunk<WM, TP, 0, false, APX>(X, B, st[s], C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax);
       __syncwarp();
       if (l == 0 && c + NSTG < nch) {
         // (no proxy fence: the stage's generic reads were all consumed by this
@@ -391,7 +408,7 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
     }
 #pragma unroll
     for (int off = 16; off; off >>= 1) t = umax64(t, __shfl_xor_sync(FULL, t, off));
-    if (l == 0) wmax[w][i] = t;
+    if (l == 0) wmax[w][i] = APX ? t << 32 : t;  // APX: the lower bound LB = H << 32
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -407,16 +424,18 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
     const unsigned tk = atomicAdd(&A.ctl->ticket, 1u);
     if (tk == gridDim.x - 1) {
       A.ctl->ticket = 0;
-      // first of the WM iterations that stops the solve (same test as sor_decide)
+      // first of the WM iterations that stops the solve (same test as sor_decide;
+      // APX: on the lower bound LB <= rho, so every true stop is caught and marked
+      // provisional (status 4) -- as is LB = +Inf, which may hide a NaN)
       for (int i = 0; i < WM; ++i) {
         const int k = A.k + i;
         const unsigned long long rb = atomicAdd(&A.rho_bits[k], 0ull);
         const double rho = __longlong_as_double((long long)rb);
-        const bool nan_ = isnan(rho);
+        const bool nan_ = isnan(rho) || (APX && (rb >> 32) == 0x7ff00000ull);
         const bool conv = (k % A.check_every == 0) && rho <= A.tol;
         if (nan_ || conv || k >= A.maxit) {
           A.ctl->rho_final = rb;
-          A.ctl->status = nan_ ? 3 : (conv ? 0 : 1);
+          A.ctl->status = APX ? 4 : (nan_ ? 3 : (conv ? 0 : 1));
           __threadfence();
           A.ctl->k_done = k;
           break;
@@ -426,27 +445,37 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
   }
 }
 
-template <int WM, int TP>
+template <int WM, int TP, bool APX>
 int wf_blocks_per_sm() {
   static int per = 0;
   if (!per) {
-    cudaFuncSetAttribute(k_sor_wf<WM, TP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wf_smem<WM>());
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sor_wf<WM, TP>, WNT, wf_smem<WM>());
+    cudaFuncSetAttribute(k_sor_wf<WM, TP, APX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wf_smem<WM>());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sor_wf<WM, TP, APX>, WNT, wf_smem<WM>());
     if (per < 1) per = 1;
   }
   return per;
 }
 
-template <int WM>
-cudaError_t wf_launch(const WfArgs &a, cudaStream_t s) {
+template <int WM, bool APX>
+void wf_launch_tp(const WfArgs &a, cudaStream_t s) {
   const int grid = (a.items + WNW - 1) / WNW;
   if (a.g.gj0 & 1) {
-    wf_blocks_per_sm<WM, 1>();
-    k_sor_wf<WM, 1><<<grid, WNT, wf_smem<WM>(), s>>>(a);
+    wf_blocks_per_sm<WM, 1, APX>();
+    k_sor_wf<WM, 1, APX><<<grid, WNT, wf_smem<WM>(), s>>>(a);
   } else {
-    wf_blocks_per_sm<WM, 0>();
-    k_sor_wf<WM, 0><<<grid, WNT, wf_smem<WM>(), s>>>(a);
+    wf_blocks_per_sm<WM, 0, APX>();
+    k_sor_wf<WM, 0, APX><<<grid, WNT, wf_smem<WM>(), s>>>(a);
   }
+}
+
+// approximate residual on single-slab solves (decision on the device); exact on
+// decomposed ones (the cross-slab reduction and k_sor_check take exact words)
+template <int WM>
+cudaError_t wf_launch(const WfArgs &a, cudaStream_t s) {
+  if (a.multi)
+    wf_launch_tp<WM, false>(a, s);
+  else
+    wf_launch_tp<WM, true>(a, s);
   return cudaGetLastError();
 }
 

@@ -122,3 +122,29 @@ def test_loopback_cylinder_fused(mods, wf_rows, m):
     cfg = I.cfg2(nx=96, ny=72, steps=3, maxit_p=400)
     o, g, ro, rg = run_pair(mods, cfg, cfg.steps, nranks=2, loopback=True, sor_fuse=m)
     assert_parity(o, g, ro, rg)
+
+
+@pytest.mark.parametrize("m", FUSE)
+@pytest.mark.parametrize("K", [37, 38, 39])
+def test_provisional_stop_not_confirmed(mods, wf_rows, m, K):
+    """The fused pass decides on a lower bound of rho (its high 32 bits).  With
+    tol set to that bound at iteration K (taken from the oracle: rho_K with its
+    low word cleared, < rho_K), the pass holding K stops provisionally, the exact
+    replay finds rho_K > tol and the solve carries on -- to the oracle's own stop."""
+    import struct
+    O, P = mods
+    wf_rows(0)
+    probe = I.cfg1(nx=64, ny=48, steps=1, maxit_p=K)
+    o = O.Oracle(probe.xn, probe.yn, **probe.solver_kwargs())
+    o.set_body(*probe.body_args())
+    o.set_fields(*I.initial_fields(probe.nx, probe.ny, probe.perturb))
+    _, st = o.step(1)
+    assert st[0, 2] == K
+    bits = struct.unpack("<Q", struct.pack("<d", st[0, 4]))[0]
+    assert bits & 0xFFFFFFFF, "rho_K has an empty low word: pick another K"
+    tol = struct.unpack("<d", struct.pack("<Q", bits & ~0xFFFFFFFF))[0]
+    cfg = I.cfg1(nx=64, ny=48, steps=1, tol_p=tol, maxit_p=5000)
+    o2, g, ro, rg = run_pair(mods, cfg, cfg.steps, sor_batch=4, sor_fuse=m)
+    assert ro[1][0, 2] > K  # the oracle goes past K
+    assert_parity(o2, g, ro, rg)
+    g.close()
