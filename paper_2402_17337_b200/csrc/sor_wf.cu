@@ -288,7 +288,6 @@ template <int WM, int TP, bool APX>
 __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __grid_constant__ WfArgs A) {
   constexpr int W = 2 * WM + 2, OW = SC - 4 * WM, NSTG = wf_nstg<WM>();
   constexpr unsigned kBytes = 2u * W * SC * 8;
-  if (*(volatile int *)&A.ctl->k_done >= 0) return;  // converged at an earlier iteration
   extern __shared__ __align__(1024) unsigned char smraw[];
   __shared__ unsigned long long wmax[WNW][WM];
   const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -301,6 +300,7 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
 #pragma unroll
     for (int s = 0; s < NS; ++s) tmax[i][s] = 0ull;
   const int item = blockIdx.x * WNW + w;
+  if (item >= A.items && *(volatile int *)&A.ctl->k_done >= 0) return;  // (working warps: below)
   if (item < A.items) {
     const Geo &g = A.g;
     const int sx = item % A.strips, sy = item / A.strips;
@@ -319,6 +319,13 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
       }
     }
     __syncwarp();
+    // converged at an earlier iteration: nothing to do.  Tested after the first
+    // TMA issue so that the control-word round trip does not delay the item's
+    // first chunk; the loads in flight are waited for before leaving.
+    if (*(volatile int *)&A.ctl->k_done >= 0) {
+      for (int c = 0; c < NSTG && c < nch; ++c) mbar_wait_warp(&bar[c], 0);
+      return;
+    }
     bool lane_own[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
