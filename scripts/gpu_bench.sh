@@ -15,7 +15,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 # first step, the one-iteration pass (--sor-fuse 1) likewise, and the other kernels
 ncu --set full --clock-control none --import-source on -k regex:k_sor_wf -s 40 -c 1 -o gpurun_out/prof_wf_${TAG} -f \
     python bench.py --steps 1 --warmup 0 --maxit-p 220 --no-e2e --no-cpu-baseline --no-clocks --sor-batch 256 > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:'k_sor<0' -s 40 -c 1 -o gpurun_out/prof_sor_${TAG} -f \
+ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:'k_sor<.int.0' -s 40 -c 1 -o gpurun_out/prof_sor_${TAG} -f \
     python bench.py --steps 1 --warmup 0 --maxit-p 220 --no-e2e --no-cpu-baseline --no-clocks --sor-batch 256 --sor-fuse 1 > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:'k_pred|k_prhs|k_correct|k_classify|k_pflags|k_forces' -c 12 \
     -o gpurun_out/prof_other_${TAG} -f python bench.py --steps 1 --warmup 0 --maxit-p 5 --maxit-uv 3 --no-e2e --no-cpu-baseline --no-clocks --sor-batch 256 > /dev/null 2>&1
