@@ -98,7 +98,10 @@ typedef struct {
     int it_uv, it_p;            /* SOR iterations of the velocity / pressure solves */
     double rho_uv, rho_p;       /* final max-norm update |gs - x_old| (reading R2) */
     double cd, cl;              /* force coefficients of this step */
-    float ms[6];                /* device ms: classify+predictor, uv-SOR, rhs, p-SOR, correct, forces */
+    float ms[8];                /* device ms (CUDA events on the solver stream): [0] classify+predictor,
+                                   [1] uv-SOR (+ outlet fill), [2] Poisson rhs, [3] p-SOR, [4] correct,
+                                   [5] forces, [6] of [0]: classification and Poisson masks (a1, the
+                                   paper's "flagging", Table 1), [7] whole step */
     int status;                 /* IBM_OK / IBM_WARN_NOCONV / IBM_ERR_DIVERGED */
     int launches;               /* CUDA kernels this library launched for the step (incl.
                                    early-exit SOR iterations past convergence) */

@@ -29,9 +29,11 @@
  *                         mirror symmetry, zero-force cases
  *   temporal order of AB2/CN: parity unpinned.
  */
+#define _POSIX_C_SOURCE 199309L /* clock_gettime (region timers only) */
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
 
 enum { FLUID = 0, SOLID = 1, FORCING = 2 };
 enum { ORC_OK = 0, ORC_WARN_NOCONV = 1, ORC_ERR_CONFIG = 2, ORC_ERR_DIVERGED = 3 };
@@ -62,12 +64,30 @@ typedef struct {
     double t, yb, vb, cd, cl;
     int it_uv, it_p;
     double rho_uv, rho_p;
+    /* region wall times (s), accumulated over steps, in the layout of the paper's
+     * Table 1: flagging, predictor + forcing, U-V solver, Poisson rhs,
+     * P solver, correction, forces.  Timing only: no effect on the arithmetic. */
+    double tm[7];
 } orc_ctx;
 
 /* ---------------- indexing ---------------- */
 #define UI(c, i, j) ((size_t)(j) * (size_t)((c)->nx + 1) + (size_t)(i))
 #define VI(c, i, j) ((size_t)(j) * (size_t)(c)->nx + (size_t)(i))
 #define PI_(c, i, j) ((size_t)(j) * (size_t)(c)->nx + (size_t)(i))
+
+static double now_s(void)
+{
+    struct timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+}
+/* adds the time since *t0 to region r and restarts the clock */
+static void tick(orc_ctx *c, int r, double *t0)
+{
+    double t = now_s();
+    c->tm[r] += t - *t0;
+    *t0 = t;
+}
 
 static double *dalloc(size_t n) { return (double *)calloc(n ? n : 1, sizeof(double)); }
 static unsigned char *balloc(size_t n) { return (unsigned char *)calloc(n ? n : 1, 1); }
@@ -559,6 +579,7 @@ static int step_once(orc_ctx *c)
     const double dt = c->dt;
     const double halfnu = 0.5 / c->Re, nu_ = 1.0 / c->Re, beta = dt * halfnu;
     int status = ORC_OK, st;
+    double t0 = now_s();
 
     /* a0: t^{n+1} = (n+1) dt, body at t^{n+1} (R13, R15) ; a1: classification */
     c->t = (double)(c->step + 1) * dt;
@@ -567,6 +588,7 @@ static int step_once(orc_ctx *c)
     /* a5 masks (R16-R18) depend only on the tags, so they are built here: the
      * predictor's pressure gradient at Fluid nodes uses open faces only (R9b) */
     build_masks(c);
+    tick(c, 0, &t0);
 
     /* a2: convection C^n at Fluid+Forcing nodes; first step Euler (R8) */
     convection(c, c->u, c->v, c->cu, c->cv);
@@ -615,6 +637,7 @@ static int step_once(orc_ctx *c)
             }
         }
 
+    tick(c, 1, &t0);
     /* a4: CN Helmholtz (I - beta L) u* = rhs, u and v jointly by red-black SOR (R5, R6) */
     {
         double *aPu = dalloc(nu), *aEu = dalloc(nu), *aWu = dalloc(nu), *aNu = dalloc(nu), *aSu = dalloc(nu);
@@ -655,6 +678,7 @@ static int step_once(orc_ctx *c)
         c->us[UI(c, nx, j)] = c->us[UI(c, nx - 1, j)] -
                               c->dx[nx - 1] * ((c->vs[VI(c, nx - 1, j + 1)] - c->vs[VI(c, nx - 1, j)]) / c->dy[j]);
 
+    tick(c, 2, &t0);
     /* a5: mass source q and Poisson rhs on the masks built above (R16) */
     for (int j = 0; j < ny; ++j)
         for (int i = 0; i < nx; ++i) {
@@ -672,11 +696,13 @@ static int step_once(orc_ctx *c)
             c->bp[id] = -rhs;
         }
 
+    tick(c, 3, &t0);
     /* a6: Poisson red-black SOR, warm start phi^{n-1}, phi = 0 on inactive cells (R6, R17) */
     c->it_p = poisson_solve(c, c->bp, c->phi, &c->rho_p, &st);
     if (st == ORC_ERR_DIVERGED) return ORC_ERR_DIVERGED;
     if (st == ORC_WARN_NOCONV) status = ORC_WARN_NOCONV;
 
+    tick(c, 4, &t0);
     /* a7: projection / correction (R9, R16, R17) */
     for (int j = 0; j < ny; ++j)
         for (int i = 0; i <= nx; ++i) {
@@ -707,6 +733,7 @@ static int step_once(orc_ctx *c)
     memcpy(c->cv_prev, c->cv, nv * sizeof(double));
     c->have_hist = 1;
 
+    tick(c, 5, &t0);
     /* a8: forces, S:352-360 (R20) */
     {
         double sfx = 0.0, sfy = 0.0;
@@ -728,6 +755,7 @@ static int step_once(orc_ctx *c)
 
     c->step += 1;
 
+    tick(c, 6, &t0);
     /* NaN guard */
     for (size_t id = 0; id < nu; ++id) if (!isfinite(c->u[id])) return ORC_ERR_DIVERGED;
     for (size_t id = 0; id < nv; ++id) if (!isfinite(c->v[id])) return ORC_ERR_DIVERGED;
@@ -775,6 +803,12 @@ int orc_get_tags(const orc_ctx *c, int which, unsigned char *out)
     if (which < 0 || which > 5) return ORC_ERR_CONFIG;
     memcpy(out, src[which], n[which]);
     return ORC_OK;
+}
+
+/* accumulated region times (s) since the last call, Table 1 layout (see orc_ctx.tm); resets them */
+void orc_timers(orc_ctx *c, double *out7)
+{
+    for (int r = 0; r < 7; ++r) { out7[r] = c->tm[r]; c->tm[r] = 0.0; }
 }
 
 void orc_forces(const orc_ctx *c, double *out3)

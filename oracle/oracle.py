@@ -63,6 +63,7 @@ def lib():
         L.orc_get_tags.argtypes = [vp, i, bp]
         L.orc_get_tags.restype = i
         L.orc_forces.argtypes = [vp, dp]
+        L.orc_timers.argtypes = [vp, dp]
         L.orc_classify_at.argtypes = [vp, d]
         L.orc_convection.argtypes = [vp, dp, dp, dp, dp]
         L.orc_laplacian.argtypes = [vp, i, dp, dp]
@@ -173,6 +174,13 @@ class Oracle:
             return out
         out = np.zeros(self.shape(name))
         lib().orc_get(self._c, FIELDS[name], out)
+        return out
+
+    def timers(self):
+        """Region wall times (s) since the last call: flagging, predictor+forcing, U-V SOR,
+        Poisson rhs, P SOR, correction, forces (Table 1 layout)."""
+        out = np.zeros(7)
+        lib().orc_timers(self._c, out)
         return out
 
     def forces(self):

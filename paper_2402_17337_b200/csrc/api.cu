@@ -664,6 +664,7 @@ int step_once(Ctx &c, ibm_step_stats *st) {
       c.launches += launch_classify(c, s, yb);
       c.launches += launch_pflags(c, s);
     }
+  CK(cudaEventRecord(c.ev[7], c.stream));
   // N1 halos of u^n, v^n, p^n, then a2/a3 predictor
   if (multi(c)) {
     HALO((*b = s.u, *g = &s.gu));
@@ -745,6 +746,8 @@ int step_once(Ctx &c, ibm_step_stats *st) {
     st->ms[3] = ev_ms(c, 3, 4);
     st->ms[4] = ev_ms(c, 4, 5);
     st->ms[5] = ev_ms(c, 5, 6);
+    st->ms[6] = ev_ms(c, 0, 7);
+    st->ms[7] = ev_ms(c, 0, 6);
     st->launches = c.launches;
   }
   if (*c.h_nan) {

@@ -51,7 +51,7 @@ class ibm_config(C.Structure):
 class ibm_step_stats(C.Structure):
     _fields_ = [("step", C.c_int), ("t_bar", C.c_double), ("it_uv", C.c_int), ("it_p", C.c_int),
                 ("rho_uv", C.c_double), ("rho_p", C.c_double), ("cd", C.c_double), ("cl", C.c_double),
-                ("ms", C.c_float * 6), ("status", C.c_int), ("launches", C.c_int)]
+                ("ms", C.c_float * 8), ("status", C.c_int), ("launches", C.c_int)]
 
 
 EXPORTS = ["ibm_workspace_size", "ibm_nccl_unique_id", "ibm_init", "ibm_set_body", "ibm_clear_body",

@@ -1,0 +1,113 @@
+"""performance report in the layout of the paper's Table 1
+(serial per-function times of one step) and Table 2,
+for the CPU oracle (one core: the analogue of the paper's serial SOL0) and the
+B200 path, on the same configuration and the same iteration counts.
+
+Regions (oracle: `Oracle.timers()`, wall clock per region; GPU: the CUDA-event
+phase times of `ibm_step_stats.ms`):
+  flagging            a1 classification + Poisson masks   (Table 1 "fluid/solid flagging")
+  predictor+forcing   a2/a3 convection, Helmholtz rhs, IBM forcing targets
+                      (contains Table 1's "body-force interpolation")
+  U-V solver          a4 Helmholtz red-black SOR + outlet fill
+  Poisson rhs         a5
+  P solver            a6 Poisson red-black SOR
+  correction          a7 projection + history rotation
+  forces              a8
+Amdahl: S(n) = 1 / ((1 - p) + p / n) with the paper's p = 0.998 gives
+S_inf = 500; the measured whole-step ratio oracle / GPU is printed beside it.
+
+Usage: python scripts/perf_report.py [--level 1] [--maxit-p 200] [--oracle-steps 2]
+                                     [--gpu-steps 20] [--out profiles/r01_perf_report]"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import ibm_inputs as I  # noqa: E402
+
+REGIONS = ["flagging", "predictor+forcing", "U-V solver", "Poisson rhs", "P solver", "correction", "forces"]
+# Table 1, seconds per step, SOL0 serial, i7 10th gen; mesh not stated
+PAPER_T1 = {"P solver": 3.835, "flagging": 2.5515, "U-V solver": 0.5518, "body-force interpolation": 0.0758}
+PAPER_P = 0.998
+
+
+def gpu_regions(ms):
+    """ibm_step_stats.ms -> region seconds: [0] classify+predictor, [1] uv, [2] rhs, [3] p, [4] correct,
+    [5] forces, [6] classification part of [0]."""
+    return np.array([ms[6], ms[0] - ms[6], ms[1], ms[2], ms[3], ms[4], ms[5]]) / 1e3
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--level", type=int, default=1)
+    ap.add_argument("--maxit-p", type=int, default=200)
+    ap.add_argument("--oracle-steps", type=int, default=2)
+    ap.add_argument("--gpu-steps", type=int, default=20)
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_perf_report"))
+    args = ap.parse_args()
+    from oracle import oracle as O
+    import paper_2402_17337_b200 as P
+
+    cfg = I.cfg3(level=args.level, steps=args.oracle_steps, maxit_p=args.maxit_p)
+    u0, v0, p0 = I.initial_fields(cfg.nx, cfg.ny)
+    # oracle (single thread): the first oracle_steps steps
+    o = O.Oracle(cfg.xn, cfg.yn, **cfg.solver_kwargs())
+    o.set_body(*cfg.body_args())
+    o.set_fields(u0, v0, p0)
+    t0 = time.time()
+    _, sto = o.step(args.oracle_steps)
+    o_wall = (time.time() - t0) / args.oracle_steps
+    o_reg = o.timers() / args.oracle_steps
+    # GPU: the same first steps (identical iteration counts), then more steps for a stable mean
+    g = P.Solver(cfg.xn, cfg.yn, **cfg.solver_kwargs())
+    g.set_body(*cfg.body_args())
+    g.set_fields(u0, v0, p0)
+    _, stg = g.step(args.oracle_steps)
+    assert np.array_equal(stg[:, 1:3], sto[:, 1:3]), "iteration counts differ from the oracle"
+    _, stg2 = g.step(args.gpu_steps)
+    raw = g.last_stats
+    g_reg = np.mean([gpu_regions(raw[k].ms) for k in range(args.gpu_steps)], axis=0)
+    g_step = float(np.mean([raw[k].ms[7] for k in range(args.gpu_steps)])) / 1e3
+    g.close()
+    rows = []
+    for name, a, b in zip(REGIONS, o_reg, g_reg):
+        rows.append({"region": name, "oracle_s": float(a), "oracle_pct": float(100 * a / o_reg.sum()),
+                     "gpu_ms": float(1e3 * b), "gpu_pct": float(100 * b / g_reg.sum()),
+                     "speedup": float(a / b) if b > 0 else None, "paper_sol0_s": PAPER_T1.get(name)})
+    S = float(o_reg.sum() / g_reg.sum())
+    res = {"config": {"workload": cfg.name, "nx": cfg.nx, "ny": cfg.ny, "maxit_p": args.maxit_p,
+                      "it_p_per_step": stg2[:, 2].tolist()[:3], "it_uv_per_step": stg2[:, 1].tolist()[:3]},
+           "oracle": {"cores": 1, "wall_s_per_step": o_wall, "regions_s_per_step": float(o_reg.sum())},
+           "gpu": {"device": "B200", "step_ms": 1e3 * g_step, "regions_ms": float(1e3 * g_reg.sum())},
+           "rows": rows, "speedup_whole_step": S,
+           "amdahl_paper": {"p": PAPER_P, "S_inf": 1.0 / (1.0 - PAPER_P)},
+           "paper_table1_note": "Table 1 is SOL0 on an unstated mesh (P:109-112): shares, not seconds, compare",
+           "paper_sol0_shares_pct": {k: 100 * v / 7.014 for k, v in PAPER_T1.items()}}
+    os.makedirs(os.path.dirname(args.out), exist_ok=True)
+    json.dump(res, open(args.out + ".json", "w"), indent=1)
+    lines = ["# Performance report (SURVEY §8(f) f4): %s, %d x %d, maxit_p = %d" % (cfg.name, cfg.nx, cfg.ny,
+                                                                                       args.maxit_p), "",
+             "Oracle = plain C, one core of the GPU box's host (SOL0 analogue); GPU = this build on one B200.",
+             "Same configuration and identical iteration counts (asserted).  Paper SOL0 shares from Table 1",
+             "(P:109-112, total 7.014 s over its four hotspots, mesh unstated) for comparison of SHARES.", "",
+             "| region | oracle s/step | oracle % | GPU ms/step | GPU % | speedup | paper SOL0 % |",
+             "|---|---|---|---|---|---|---|"]
+    for r in rows:
+        ps = res["paper_sol0_shares_pct"].get(r["region"])
+        lines.append("| %s | %.4f | %.1f | %.3f | %.1f | %s | %s |" % (
+            r["region"], r["oracle_s"], r["oracle_pct"], r["gpu_ms"], r["gpu_pct"],
+            "%.0f" % r["speedup"] if r["speedup"] else "-", "%.1f" % ps if ps is not None else "-"))
+    lines += ["", "Whole step: oracle %.3f s, GPU %.3f ms, ratio %.0f.  Amdahl with the paper's p = %.3f (P:101): "
+              "S_inf = %.0f." % (o_reg.sum(), 1e3 * g_reg.sum(), S, PAPER_P, 1.0 / (1.0 - PAPER_P))]
+    open(args.out + ".md", "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
+if __name__ == "__main__":
+    main()
