@@ -301,3 +301,17 @@ def test_persistent_and_launched_sor_agree(mods):
     assert np.array_equal(out[0][1][:, 1:5], out[1][1][:, 1:5])
     for n in ("u", "v", "p", "phi"):
         assert np.array_equal(out[0][2][n], out[1][2][n]), n
+
+
+@pytest.mark.parametrize("sor_batch", [0, 8])
+def test_production_mesh_m1_parity(mods, sor_batch):
+    """BJ configs[2] shape: the paper's stretched production mesh M1 (997 x 602,
+    reading R28), foil at Re = 500, dt = 1e-4, impulsive start; 2 steps with the
+    Poisson solve capped at 150 iterations so that the oracle finishes in seconds.
+    sor_batch = 0: the automatic path (persistent cooperative solve at this size);
+    8: host-batched one-iteration passes.  Bit-identical fields, equal iteration
+    counts, forces within the BJ bar."""
+    cfg = I.cfg3(level=1, steps=2, maxit_p=150)
+    o, g, ro, rg = run_pair(mods, cfg, cfg.steps, sor_batch=sor_batch)
+    assert_parity(o, g, ro, rg)
+    g.close()
