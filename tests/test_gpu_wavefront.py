@@ -148,3 +148,23 @@ def test_provisional_stop_not_confirmed(mods, wf_rows, m, K):
     assert ro[1][0, 2] > K  # the oracle goes past K
     assert_parity(o2, g, ro, rg)
     g.close()
+
+
+@pytest.mark.parametrize("m", FUSE)
+def test_nan_in_fused_poisson_is_divergence(mods, wf_rows, m):
+    """A NaN that first appears in the Poisson solve (warm-start phi) is caught by
+    the fused pass's approximate residual (high word 0x7fffffff), confirmed by the
+    exact replay, and reported as divergence -- as by the one-iteration pass."""
+    O, P = mods
+    wf_rows(0)
+    cfg = I.cfg1(nx=64, ny=48, steps=1, maxit_p=200)
+    u0, v0, p0 = I.initial_fields(cfg.nx, cfg.ny, cfg.perturb)
+    phi0 = np.zeros((cfg.ny, cfg.nx))
+    phi0[20, 30] = np.nan
+    for fuse in (1, m):
+        g = P.Solver(cfg.xn, cfg.yn, sor_batch=4, sor_fuse=fuse, **cfg.solver_kwargs())
+        g.set_body(*cfg.body_args())
+        g.set_fields(u0, v0, p0, phi=phi0)
+        st, _ = g.step(1)
+        assert st == 3, (fuse, st)
+        g.close()
