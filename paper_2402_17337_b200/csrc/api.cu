@@ -6,6 +6,7 @@
 // the uint64 bit pattern, exact); in loopback mode (test) all slabs live in one
 // ctx and the same exchanges are device-to-device copies.  Everything stays in
 // HBM; per step only the SOR control words and 4 force sums reach the host.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -553,12 +554,34 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
   int &hint = helm ? c.hint_uv : c.hint_p;
   int batch = cfg.sor_batch > 0 ? cfg.sor_batch : std::max(4, std::min(hint, maxit));
   int k = 1, cur = s0;
+  // Online tuning of the fused pass's segment length (single slab, no
+  // IBM_WF_ROWS): the first 2 x ncand fused passes of a run cycle through the
+  // candidates (wf_candidates), each timed by its own events; the fastest is kept
+  // for the rest of the run.  Every length gives the same iterates, so these are
+  // ordinary passes of the solve.
+  std::vector<int> cand;
+  int tune_n = 0, tune_launched = 0, tune_k_end = 0;
+  if (wf && !mult) {
+    if (c.wf_L == 0 && !std::getenv("IBM_WF_ROWS")) {
+      cand = wf_candidates(c.sl[0].gp, c.wf_m);
+      if (cand.size() > 1)
+        tune_n = std::min(2 * (int)cand.size(), 6);
+      else
+        c.wf_L = cand[0];
+    }
+    if (c.wf_L > 0) wf_plan(was[0], c.wf_m, c.wf_L);
+  }
   for (;;) {
     const int kend = std::min(maxit, k + batch - 1);
     while (k <= kend) {
       if (wf && k + c.wf_m - 1 <= maxit) {
         const int in = cur;
         if (mult) HALO_ROWS(2 * c.wf_m, (*b = s.phi[in], *g = &s.gp));
+        const bool tuning = tune_launched < tune_n;
+        if (tuning) {
+          wf_plan(was[0], c.wf_m, cand[tune_launched % cand.size()]);
+          CK(cudaEventRecord(c.tev[2 * tune_launched], c.stream));
+        }
         for (size_t r = 0; r < c.sl.size(); ++r) {
           WfArgs &wa = was[r];
           wa.k = k;
@@ -566,6 +589,10 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
           wa.tmx = c.sl[r].tm_wphi[in];
           CK(launch_sor_wf(wa, c.wf_m, c.stream));
           ++c.launches;
+        }
+        if (tuning) {
+          CK(cudaEventRecord(c.tev[2 * tune_launched + 1], c.stream));
+          if (++tune_launched == tune_n) tune_k_end = k + c.wf_m - 1;
         }
         if (mult) {
           if (!c.loopback)
@@ -587,6 +614,21 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(&c.h_ctl[0], c.ctl, sizeof(SorCtl), cudaMemcpyDeviceToHost, c.stream));
     CK(cudaStreamSynchronize(c.stream));
+    if (tune_n > 0 && tune_launched == tune_n && c.wf_L == 0) {
+      // all tuning passes ran in full unless the solve stopped inside them (then
+      // the next run tunes again)
+      if (c.h_ctl[0].k_done < 0 || c.h_ctl[0].k_done >= tune_k_end) {
+        std::vector<float> best(cand.size(), 1e30f);
+        for (int i = 0; i < tune_n; ++i) {
+          float ms = 0.f;
+          if (cudaEventElapsedTime(&ms, c.tev[2 * i], c.tev[2 * i + 1]) == cudaSuccess)
+            best[i % cand.size()] = std::min(best[i % cand.size()], ms);
+        }
+        c.wf_L = cand[std::min_element(best.begin(), best.end()) - best.begin()];
+        wf_plan(was[0], c.wf_m, c.wf_L);
+      }
+      tune_n = 0;
+    }
     if (c.h_ctl[0].k_done >= 0 && c.h_ctl[0].status == 4) {
       // Provisional stop in a fused pass with the approximate (high-word) residual:
       // replay that pass from its intact input with exact one-iteration passes --
@@ -855,6 +897,9 @@ int ibm_init(const ibm_config *cfg, void *d_workspace, size_t bytes, void *cuda_
   }
   for (auto &e : c.ev)
     if (cudaEventCreate(&e) != cudaSuccess) { c.err = "cudaEventCreate failed"; return fail(IBM_ERR_CUDA); }
+  for (auto &e : c.tev)
+    if (cudaEventCreate(&e) != cudaSuccess) { c.err = "cudaEventCreate failed"; return fail(IBM_ERR_CUDA); }
+  c.wf_L = 0;
   HostMetric h = host_metric(*cfg);
   c.h_xn = nullptr;
   c.h_yn = nullptr;
@@ -1083,6 +1128,7 @@ int ibm_destroy(ibm_ctx *ctx) {
   cudaStreamSynchronize(c.stream);
   if (c.nccl) ncclCommDestroy((ncclComm_t)c.nccl);
   for (auto &e : c.ev) cudaEventDestroy(e);
+  for (auto &e : c.tev) cudaEventDestroy(e);
   cudaFreeHost(c.h_ctl);
   cudaFreeHost(c.h_red);
   cudaFreeHost(c.h_nan);

@@ -150,6 +150,8 @@ struct Ctx {
   double last_t, last_cd, last_cl;
   int hint_uv, hint_p;
   int wf_m;         // Poisson iterations fused per HBM pass (1 = unfused k_sor)
+  int wf_L;         // fused-pass segment length chosen by the online tuner (0: not yet)
+  cudaEvent_t tev[12];  // tuner: start / stop of the first fused passes of a run
   int launches;     // kernels launched in the current step
   cudaEvent_t ev[8];
   void *nccl;      // ncclComm_t when nranks > 1 and !loopback
@@ -172,7 +174,9 @@ void launch_sor_iteration(const SorArgs &a, cudaStream_t st, int grid);
 // temporally blocked Poisson pass: rows of the TMA box, segment length, launch
 int wf_box_rows(int m);
 int wf_box_cols();
-void wf_plan(WfArgs &a, int m);
+void wf_plan(WfArgs &a, int m, int L_force = 0);
+// segment lengths worth trying for this slab (the static choice first)
+std::vector<int> wf_candidates(const Geo &g, int m);
 bool wf_viable(int ni, int nj, int m);
 cudaError_t launch_sor_wf(const WfArgs &a, int m, cudaStream_t st);
 void launch_sor_check(SorCtl *ctl, const unsigned long long *rho_bits, int k, int maxit, int check_every,

@@ -27,7 +27,9 @@
 // reciprocals; the rest (domain edges, body, stretched rows) the predicated one.
 //
 // Arithmetic: identical to sor.cu (R13).
+#include <algorithm>
 #include <climits>
+#include <cmath>
 #include <cstdlib>
 #include <type_traits>
 #include <utility>
@@ -525,10 +527,30 @@ bool wf_viable(int ni, int nj, int m) {
   return (long)wf_strips(ni, m) * ((nj + wf_rows_min(m) - 1) / wf_rows_min(m)) >= wf_items_target();
 }
 
-void wf_plan(WfArgs &a, int m) {
-  a.strips = wf_strips(a.g.ni, m);
+static int wf_static_rows(const Geo &g, int m) {
+  const int strips = wf_strips(g.ni, m);
   int L = wf_rows_default(m);
-  while (L > wf_rows_min(m) && (long)a.strips * ((a.g.nj + L - 1) / L) < wf_items_target()) L /= 2;
+  while (L > wf_rows_min(m) && (long)strips * ((g.nj + L - 1) / L) < wf_items_target()) L /= 2;
+  return L;
+}
+
+// The static choice, half and twice it.  The pass time does not follow a simple
+// model in L (8192^2, m = 3: 128 and 256 fast, 160 / 192 / 224 / 240 20-30 %
+// slower, although 224 fills the last wave best), so sor_solve
+// times the first fused passes of a run with each candidate and keeps the
+// fastest; every L gives bit-identical iterates, so the tuning passes are real work.
+std::vector<int> wf_candidates(const Geo &g, int m) {
+  const int strips = wf_strips(g.ni, m);
+  const int L0 = wf_static_rows(g, m);
+  std::vector<int> c{L0};
+  if (L0 / 2 >= wf_rows_min(m)) c.push_back(L0 / 2);
+  if (2 * L0 <= 512 && (long)strips * ((g.nj + 2 * L0 - 1) / (2 * L0)) >= wf_items_target()) c.push_back(2 * L0);
+  return c;
+}
+
+void wf_plan(WfArgs &a, int m, int L_force) {
+  a.strips = wf_strips(a.g.ni, m);
+  int L = L_force > 0 ? L_force : wf_static_rows(a.g, m);
   if (const char *e = std::getenv("IBM_WF_ROWS")) {
     const int v = std::atoi(e);
     if (v > 0) L = v;
