@@ -25,6 +25,11 @@
 // all inside the family, away from the body box and carry the segment's
 // reference row coefficients take a check-free path with per-column
 // reciprocals; the rest (domain edges, body, stretched rows) the predicated one.
+// One warp per CTA (one work item), 8 per SM.
+//
+// Residual: on single-slab solves (APX) the max of the high word of |d|, a lower
+// bound of rho whose stops are provisional and confirmed by the host's exact
+// replay of the pass (sor_solve); on decomposed solves the exact 64-bit max.
 //
 // Arithmetic: identical to sor.cu (R13).
 #include <algorithm>

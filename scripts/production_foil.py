@@ -76,6 +76,7 @@ def main():
     ap.add_argument("--levels", type=int, nargs="+", default=[1, 2, 3])
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--omega-p", type=float, default=None)
+    ap.add_argument("--maxit-p", type=int, default=None)
     ap.add_argument("--chunk", type=int, default=100)
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_production"))
     args = ap.parse_args()
@@ -84,8 +85,11 @@ def main():
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     for lv in args.levels:
         kw = {} if args.omega_p is None else {"omega_p": args.omega_p}
+        if args.maxit_p is not None:
+            kw["maxit_p"] = args.maxit_p
         cfg, S, r = run_level(lv, args.steps, chunk=args.chunk, **kw)
         r["omega_p"] = cfg.omega_p
+        r["maxit_p"] = cfg.maxit_p
         res["levels"].append(r)
         np.savetxt("%s_M%d.csv" % (args.out, lv), np.c_[S[:, 0], S[:, 5], S[:, 6], S[:, 1], S[:, 2]],
                    delimiter=",", header="t_bar,cd,cl,it_uv,it_p", comments="")
