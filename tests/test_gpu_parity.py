@@ -315,3 +315,29 @@ def test_production_mesh_m1_parity(mods, sor_batch):
     o, g, ro, rg = run_pair(mods, cfg, cfg.steps, sor_batch=sor_batch)
     assert_parity(o, g, ro, rg)
     g.close()
+
+
+def test_max_size_16384(mods):
+    """BJ configs[4]'s mesh (16384^2 foil on the paper domain, 44 GB of state per
+    GPU at P = 1): the fused Poisson pass runs at the maximum size; one slab and two
+    loopback slabs (the decomposed exchange schedule) give bit-identical fields
+    and iteration counts (maxit 10: three fused passes, then one one-iteration
+    pass; the single slab decides on the approximate residual, the slabs on the
+    exact one)."""
+    O, P = mods
+    import torch
+    cfg = I.cfg5(n=16384, maxit_p=10, maxit_uv=6)
+    res = []
+    for nr in (1, 2):
+        g = P.Solver(cfg.xn, cfg.yn, nranks=nr, loopback=nr > 1, **cfg.solver_kwargs())
+        g.set_body(*cfg.body_args())
+        g.set_fields(*I.initial_fields(cfg.nx, cfg.ny))
+        st, stats = g.step(1)
+        assert st in (0, 1) and stats[0, 2] == 10
+        res.append((stats.copy(), g.get("p", device=True), g.get("phi", device=True)))
+        g.close()
+        del g
+        torch.cuda.empty_cache()
+    assert np.array_equal(res[0][0][:, 1:5], res[1][0][:, 1:5])
+    assert torch.equal(res[0][1], res[1][1]) and torch.equal(res[0][2], res[1][2])
+    assert bool(torch.isfinite(res[0][1]).all())
