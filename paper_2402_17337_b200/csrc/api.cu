@@ -598,7 +598,7 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
           if (!c.loopback)
             NK(ncclAllReduce(c.rho_bits + k, c.rho_bits + k, c.wf_m, ncclUint64, ncclMax, (ncclComm_t)c.nccl,
                              c.stream));
-          launch_sor_check(c.ctl, c.rho_bits, k, maxit, cfg.check_every, tol, c.stream, c.wf_m);
+          launch_sor_check(c.ctl, c.rho_bits, k, maxit, cfg.check_every, tol, c.stream, c.wf_m, 1);
           ++c.launches;
         }
         passes.push_back({k, c.wf_m, cur});

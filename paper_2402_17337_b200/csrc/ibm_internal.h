@@ -180,7 +180,7 @@ std::vector<int> wf_candidates(const Geo &g, int m);
 bool wf_viable(int ni, int nj, int m);
 cudaError_t launch_sor_wf(const WfArgs &a, int m, cudaStream_t st);
 void launch_sor_check(SorCtl *ctl, const unsigned long long *rho_bits, int k, int maxit, int check_every,
-                      double tol, cudaStream_t st, int m = 1);
+                      double tol, cudaStream_t st, int m = 1, int apx = 0);
 int launch_outlet_fill(const Ctx &c, const Slab &s, double *us, const double *vs);
 int launch_prhs(const Ctx &c, const Slab &s, const double *us, const double *vs, double *phi_start);
 int launch_correct(const Ctx &c, const Slab &s, const double *us, const double *vs, const double *phi);

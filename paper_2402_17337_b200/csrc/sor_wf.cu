@@ -27,9 +27,9 @@
 // reciprocals; the rest (domain edges, body, stretched rows) the predicated one.
 // One warp per CTA (one work item), 8 per SM.
 //
-// Residual: on single-slab solves (APX) the max of the high word of |d|, a lower
-// bound of rho whose stops are provisional and confirmed by the host's exact
-// replay of the pass (sor_solve); on decomposed solves the exact 64-bit max.
+// Residual (APX): the max of the high word of |d|, a lower bound of rho whose
+// stops are provisional and confirmed by the host's exact replay of the pass
+// (sor_solve) -- single-slab and decomposed solves alike.
 //
 // Arithmetic: identical to sor.cu (R13).
 #include <algorithm>
@@ -482,14 +482,16 @@ void wf_launch_tp(const WfArgs &a, cudaStream_t s) {
   }
 }
 
-// approximate residual on single-slab solves (decision on the device); exact on
-// decomposed ones (the cross-slab reduction and k_sor_check take exact words)
+// approximate residual on every solve: single slab (decision by the pass's last
+// CTA) and decomposed (max over ranks of the bounds, k_sor_check with apx = 1);
+// the exact instantiation (APX = false) is kept for experiments (WF_EXACT)
 template <int WM>
 cudaError_t wf_launch(const WfArgs &a, cudaStream_t s) {
-  if (a.multi)
-    wf_launch_tp<WM, false>(a, s);
-  else
-    wf_launch_tp<WM, true>(a, s);
+#ifdef WF_EXACT
+  wf_launch_tp<WM, false>(a, s);
+#else
+  wf_launch_tp<WM, true>(a, s);
+#endif
   return cudaGetLastError();
 }
 

@@ -124,13 +124,16 @@ def test_loopback_cylinder_fused(mods, wf_rows, m):
     assert_parity(o, g, ro, rg)
 
 
+@pytest.mark.parametrize("nr", [1, 2])
 @pytest.mark.parametrize("m", FUSE)
 @pytest.mark.parametrize("K", [37, 38, 39])
-def test_provisional_stop_not_confirmed(mods, wf_rows, m, K):
+def test_provisional_stop_not_confirmed(mods, wf_rows, m, K, nr):
     """The fused pass decides on a lower bound of rho (its high 32 bits).  With
     tol set to that bound at iteration K (taken from the oracle: rho_K with its
     low word cleared, < rho_K), the pass holding K stops provisionally, the exact
-    replay finds rho_K > tol and the solve carries on -- to the oracle's own stop."""
+    replay finds rho_K > tol and the solve carries on -- to the oracle's own stop.
+    nr = 2: the same through the decomposed path (bounds reduced across slabs,
+    k_sor_check, replay with halo exchanges)."""
     import struct
     O, P = mods
     wf_rows(0)
@@ -144,7 +147,8 @@ def test_provisional_stop_not_confirmed(mods, wf_rows, m, K):
     assert bits & 0xFFFFFFFF, "rho_K has an empty low word: pick another K"
     tol = struct.unpack("<d", struct.pack("<Q", bits & ~0xFFFFFFFF))[0]
     cfg = I.cfg1(nx=64, ny=48, steps=1, tol_p=tol, maxit_p=5000)
-    o2, g, ro, rg = run_pair(mods, cfg, cfg.steps, sor_batch=4, sor_fuse=m)
+    kw = dict(nranks=2, loopback=True) if nr > 1 else {}
+    o2, g, ro, rg = run_pair(mods, cfg, cfg.steps, sor_batch=4, sor_fuse=m, **kw)
     assert ro[1][0, 2] > K  # the oracle goes past K
     assert_parity(o2, g, ro, rg)
     g.close()
