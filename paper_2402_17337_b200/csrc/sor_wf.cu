@@ -310,7 +310,18 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
   if (item >= A.items && *(volatile int *)&A.ctl->k_done >= 0) return;  // (working warps: below)
   if (item < A.items) {
     const Geo &g = A.g;
-    const int sx = item % A.strips, sy = item / A.strips;
+    // strip-major item order (consecutive CTAs = the segments of one strip): the
+    // warps streaming at the same time cover ~resident/segs strips over the whole
+    // height; measured 5-6 % faster than segment-row-major at 8192^2 (DRAM
+    // pattern).  IBM_WF_ORDER=0: segment-row-major; 1: scattered rows.
+    int sx = item / A.segs, sy = item % A.segs;
+    if (A.order == 0) {
+      sx = item % A.strips;
+      sy = item / A.strips;
+    } else if (A.order == 1) {
+      sx = item % A.strips;
+      sy = (int)(((long)(item / A.strips) * A.order_mul) % A.segs);
+    }
     const int i0 = sx * OW - 2 * WM;  // global column of stored column 0
     const int j0 = sy * A.L;          // owned local rows [j0, j1)
     const int j1 = min(j0 + A.L, g.nj);
@@ -567,6 +578,14 @@ void wf_plan(WfArgs &a, int m, int L_force) {
   a.L = L;
   a.segs = (a.g.nj + L - 1) / L;
   a.items = a.strips * a.segs;
+  a.order = 2;
+  if (const char *e = std::getenv("IBM_WF_ORDER")) a.order = std::atoi(e);
+  a.order_mul = 1;
+  for (int mlt = a.segs / 2 + 1; mlt < a.segs; ++mlt) {  // a multiplier coprime to segs
+    int x = mlt, y = a.segs;
+    while (y) { const int t = x % y; x = y; y = t; }
+    if (x == 1) { a.order_mul = mlt; break; }
+  }
 }
 
 cudaError_t launch_sor_wf(const WfArgs &a, int m, cudaStream_t s) {
