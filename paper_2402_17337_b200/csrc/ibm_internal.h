@@ -95,7 +95,7 @@ struct WfArgs {
   const double *cE, *cW, *cD, *cN, *cS;
   int ui0, ui1, uj0, uj1;
   int strips, segs, L, items;
-  int order, order_mul;  // item -> (strip, segment) order: 2 strip-major (default), 0 row-major, 1 scattered
+  int order, order_mul, order_g;  // item -> (strip, segment) order: 2 strip-major (default), 0 row-major, 1 scattered
   int multi;            // several slabs / ranks: the decision runs after the residual reduction
   double omega, omc, tol;
   int k, maxit, check_every;

@@ -321,6 +321,11 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
     } else if (A.order == 1) {
       sx = item % A.strips;
       sy = (int)(((long)(item / A.strips) * A.order_mul) % A.segs);
+    } else if (A.order == 3) {  // groups of order_g strips, segment-row-major inside a group
+      const int gsz = A.order_g * A.segs, g0 = (item / gsz) * A.order_g, r = item % gsz;
+      const int gw = min(A.order_g, A.strips - g0);
+      sx = g0 + r % gw;
+      sy = r / gw;
     }
     const int i0 = sx * OW - 2 * WM;  // global column of stored column 0
     const int j0 = sy * A.L;          // owned local rows [j0, j1)
@@ -580,6 +585,8 @@ void wf_plan(WfArgs &a, int m, int L_force) {
   a.items = a.strips * a.segs;
   a.order = 2;
   if (const char *e = std::getenv("IBM_WF_ORDER")) a.order = std::atoi(e);
+  a.order_g = 8;
+  if (const char *e = std::getenv("IBM_WF_GROUP")) a.order_g = std::max(1, std::atoi(e));
   a.order_mul = 1;
   for (int mlt = a.segs / 2 + 1; mlt < a.segs; ++mlt) {  // a multiplier coprime to segs
     int x = mlt, y = a.segs;
