@@ -270,7 +270,7 @@ def main():
     # Poisson loop on the launch stream / passes (it_p / m per step)
     Np_local = cfg.nx * (j1 - j0)
     it_p = float(stats[:, 2].sum())
-    fuse = args.sor_fuse or 3
+    fuse = g.query("wf_m")  # what the library chose (1 = one-iteration pass on thin slabs / mid grids)
     passes = float(sum(np.ceil(stats[:, 2] / fuse)))
     avg_iter_s = (psor_ms / 1e3) / max(it_p, 1.0)
     avg_launch_s = (psor_ms / 1e3) / max(passes, 1.0)

@@ -163,6 +163,16 @@ IBM_API int ibm_forces(ibm_ctx *ctx, double out[3]);
  * phi is left as computed.  rho_out (nullable) receives the last residual. */
 IBM_API int ibm_poisson_iterate(ibm_ctx *ctx, int iters, double *rho_out);
 
+/* Launch configuration the library chose, for reporting (bench roofline labels):
+ *   IBM_QUERY_WF_M  Poisson red-black iterations per HBM pass (1 = the one-iteration
+ *                   pass k_sor, 2..4 = the temporally blocked k_sor_wf)
+ *   IBM_QUERY_WF_L  segment length (owned rows per work item) of the fused pass, 0
+ *                   until the online tuner has chosen one
+ *   IBM_QUERY_SLABS slabs held by this ctx (loopback: nranks, else 1)
+ * IBM_ERR_ARG for an unknown key or NULL pointers.  No device work. */
+enum { IBM_QUERY_WF_M = 0, IBM_QUERY_WF_L = 1, IBM_QUERY_SLABS = 2 };
+IBM_API int ibm_query(const ibm_ctx *ctx, int key, int *out);
+
 /* Human-readable cause of the last error on ctx (never NULL). */
 IBM_API const char *ibm_last_error(const ibm_ctx *ctx);
 

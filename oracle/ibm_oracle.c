@@ -26,8 +26,13 @@
  *   orc_sor_generic       16x16 Dirichlet Poisson vs dense numpy solve
  *   orc_poisson           manufactured closed form, 2nd-order decay
  *   orc_step              uniform-flow fixed point, projection identity,
- *                         mirror symmetry, zero-force cases
- *   temporal order of AB2/CN: parity unpinned.
+ *                         mirror symmetry, zero-force cases,
+ *                         temporal order (AB2/CN/projection self-convergence)
+ *   forcing_target        all four directions: linear fields through N / N2,
+ *                         brute force (bisection + polyfit) at every node
+ *   forces (a8)           Archimedes -V grad p, viscous 2V/Re of u = y^2,
+ *                         cancellation for a body started from rest, discrete
+ *                         momentum budget (tests/test_oracle_force_pins.py)
  */
 #define _POSIX_C_SOURCE 199309L /* clock_gettime (region timers only) */
 #include <math.h>
@@ -254,7 +259,9 @@ void orc_classify_at(orc_ctx *c, double t)
     classify_family(c, 2, c->yb, c->tp);
 }
 
-/* ---------------- convection, S:233-241 (R7) ---------------- */
+/* ---------------- convection, S:233-241 (R7) ----------------
+ * Evaluated at every interior node, Solid ones included: C at a Solid node only
+ * enters u_hat of the momentum forcing there (R19b), never a Fluid row. */
 static void convection(const orc_ctx *c, const double *u, const double *v, double *cu, double *cv)
 {
     int nx = c->nx, ny = c->ny;
@@ -266,7 +273,6 @@ static void convection(const orc_ctx *c, const double *u, const double *v, doubl
 #define V(i, j) v[VI(c, i, j)]
     for (int j = 0; j < ny; ++j)
         for (int i = 1; i <= nx - 1; ++i) {
-            if (c->tu[UI(c, i, j)] == SOLID) continue;
             double ue = 0.5 * (U(i, j) + U(i + 1, j));
             double uw = 0.5 * (U(i - 1, j) + U(i, j));
             double tn, ts;
@@ -286,7 +292,6 @@ static void convection(const orc_ctx *c, const double *u, const double *v, doubl
         }
     for (int j = 1; j <= ny - 1; ++j)
         for (int i = 0; i < nx; ++i) {
-            if (c->tv[VI(c, i, j)] == SOLID) continue;
             double vn = 0.5 * (V(i, j) + V(i, j + 1));
             double vs = 0.5 * (V(i, j - 1) + V(i, j));
             double ue = (dy[j] * U(i + 1, j - 1) + dy[j - 1] * U(i + 1, j)) / (dy[j - 1] + dy[j]);
@@ -306,6 +311,12 @@ static void convection(const orc_ctx *c, const double *u, const double *v, doubl
 }
 
 /* ---------------- generic red-black SOR, S:278-286 (R1-R5) ---------------- */
+/* 0: the arithmetic contract R13 (default, what the GPU evaluates); 1: the plain
+ * IEEE form of SURVEY 8(c), kept only so a pin can show that the contract is a
+ * rounding choice (tests/test_oracle_pins.py::test_sor_contract_vs_plain_ieee) */
+static int g_sor_plain = 0;
+void orc_set_sor_form(int plain) { g_sor_plain = plain ? 1 : 0; }
+
 typedef struct {
     int ni, nj;
     double *x;
@@ -342,15 +353,24 @@ static int sor_run(int nsys, sor_sys *sys, double omega, double tol, int maxit,
                         double xW = fv_at(S->x, S->ni, S->nj, i - 1, j);
                         double xN = fv_at(S->x, S->ni, S->nj, i, j + 1);
                         double xS = fv_at(S->x, S->ni, S->nj, i, j - 1);
-                        /* R13: b + sum of the neighbour terms as a chain of fused multiply-adds
-                         * (C99 fma, one rounding each), S, W, E, N */
-                        double num = fma(S->aN[id], xN, fma(S->aE[id], xE, fma(S->aW[id], xW,
-                                         fma(S->aS[id], xS, S->b[id]))));
-                        double rcp = 1.0 / S->aP[id];
-                        double xo = S->x[id];
-                        double d = fma(num, rcp, -xo); /* gs - x_old, gs = num * rcp (R13) */
+                        double xo = S->x[id], d;
+                        if (!g_sor_plain) {
+                            /* R13: b + sum of the neighbour terms as a chain of fused multiply-adds
+                             * (C99 fma, one rounding each), S, W, E, N */
+                            double num = fma(S->aN[id], xN, fma(S->aE[id], xE, fma(S->aW[id], xW,
+                                             fma(S->aS[id], xS, S->b[id]))));
+                            double rcp = 1.0 / S->aP[id];
+                            d = fma(num, rcp, -xo); /* gs - x_old, gs = num * rcp (R13) */
+                            S->x[id] = fma(omega, d, xo);
+                        } else {
+                            /* SURVEY 8(c) plain IEEE form (cross-check only, never the
+                             * contract): s, gs = (b + s)/aP, x = (1-w) x + w gs */
+                            double sn = (S->aE[id] * xE + S->aW[id] * xW) + (S->aN[id] * xN + S->aS[id] * xS);
+                            double gs = (S->b[id] + sn) / S->aP[id];
+                            d = gs - xo;
+                            S->x[id] = (1.0 - omega) * xo + omega * gs;
+                        }
                         double e = fabs(d);
-                        S->x[id] = fma(omega, d, xo);
                         if (isnan(e) || isnan(rho)) rho = NAN;
                         else if (e > rho) rho = e;
                     }
@@ -609,13 +629,13 @@ static int step_once(orc_ctx *c)
             if (c->tu[id] == FLUID) {
                 if (!c->open_u[id]) G = 0.0; /* R9b: closed (solid-adjacent) face, Neumann */
                 c->rhs_u[id] = c->u[id] + dt * ((-(1.5 * C - 0.5 * Cp) - G) + halfnu * Lu);
-            } else if (c->tu[id] == FORCING) {
-                double tgt = forcing_target(c, 0, c->u, c->tu, i, j, 0.0);
+            } else {
+                /* R19b: Forcing nodes take the target, Solid nodes the body velocity; the
+                 * momentum forcing f = (u*_prescribed - u_hat)/dt is recorded at both */
+                double tgt = (c->tu[id] == FORCING) ? forcing_target(c, 0, c->u, c->tu, i, j, 0.0) : 0.0;
                 double uhat = c->u[id] + dt * ((-(1.5 * C - 0.5 * Cp) - G) + nu_ * Lu);
                 c->us[id] = tgt;
                 c->fu[id] = (tgt - uhat) / dt;
-            } else {
-                c->us[id] = 0.0;
             }
         }
     for (int j = 1; j <= ny - 1; ++j)
@@ -627,13 +647,11 @@ static int step_once(orc_ctx *c)
             if (c->tv[id] == FLUID) {
                 if (!c->open_v[id]) G = 0.0; /* R9b */
                 c->rhs_v[id] = c->v[id] + dt * ((-(1.5 * C - 0.5 * Cp) - G) + halfnu * Lv);
-            } else if (c->tv[id] == FORCING) {
-                double tgt = forcing_target(c, 1, c->v, c->tv, i, j, c->vb);
+            } else {  /* R19b */
+                double tgt = (c->tv[id] == FORCING) ? forcing_target(c, 1, c->v, c->tv, i, j, c->vb) : c->vb;
                 double vhat = c->v[id] + dt * ((-(1.5 * C - 0.5 * Cp) - G) + nu_ * Lv);
                 c->vs[id] = tgt;
                 c->fv[id] = (tgt - vhat) / dt;
-            } else {
-                c->vs[id] = c->vb;
             }
         }
 
@@ -727,6 +745,23 @@ static int step_once(orc_ctx *c)
         }
     for (size_t id = 0; id < np; ++id)
         if (c->act[id]) c->p[id] = c->p[id] + c->phi[id];
+    /* R17b: an inactive cell with at least one active 4-neighbour takes the mean of
+     * their p^{n+1} (E, W, N, S order, left fold); deeper inactive cells keep p.  Reads
+     * active cells only, so the result does not depend on the loop order. */
+    for (int j = 0; j < ny; ++j)
+        for (int i = 0; i < nx; ++i) {
+            if (c->act[PI_(c, i, j)]) continue;
+            static const int di[4] = {1, -1, 0, 0}, dj[4] = {0, 0, 1, -1};
+            double sum = 0.0;
+            int cnt = 0;
+            for (int d = 0; d < 4; ++d) {
+                int in_ = i + di[d], jn = j + dj[d];
+                if (in_ < 0 || jn < 0 || in_ >= nx || jn >= ny || !c->act[PI_(c, in_, jn)]) continue;
+                sum = sum + c->p[PI_(c, in_, jn)];
+                cnt = cnt + 1;
+            }
+            if (cnt > 0) c->p[PI_(c, i, j)] = sum / (double)cnt;
+        }
 
     /* history rotation */
     memcpy(c->cu_prev, c->cu, nu * sizeof(double));
@@ -734,15 +769,17 @@ static int step_once(orc_ctx *c)
     c->have_hist = 1;
 
     tick(c, 5, &t0);
-    /* a8: forces, S:352-360 (R20) */
+    /* a8: forces, S:352-360 (R20, R19b): F = -sum_{Solid u Forcing} f dV + (M^{n+1} - M^n)/dt,
+     * the forcing summed over every node where the scheme replaces the momentum
+     * equation, consistently with M (for unchanged tags F = sum_body (u_hat - u^n)/dt dV) */
     {
         double sfx = 0.0, sfy = 0.0;
         for (int j = 0; j < ny; ++j)
             for (int i = 1; i <= nx - 1; ++i)
-                if (c->tu[UI(c, i, j)] == FORCING) sfx = sfx + c->fu[UI(c, i, j)] * (c->hxc[i] * c->dy[j]);
+                if (c->tu[UI(c, i, j)] != FLUID) sfx = sfx + c->fu[UI(c, i, j)] * (c->hxc[i] * c->dy[j]);
         for (int j = 1; j <= ny - 1; ++j)
             for (int i = 0; i < nx; ++i)
-                if (c->tv[VI(c, i, j)] == FORCING) sfy = sfy + c->fv[VI(c, i, j)] * (c->dx[i] * c->hyc[j]);
+                if (c->tv[VI(c, i, j)] != FLUID) sfy = sfy + c->fv[VI(c, i, j)] * (c->dx[i] * c->hyc[j]);
         double Mx1, My1;
         solid_momentum(c, &Mx1, &My1);
         double Fx = -sfx + (Mx1 - c->Mx) / dt;

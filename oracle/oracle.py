@@ -74,6 +74,7 @@ def lib():
         L.orc_sor_generic.argtypes = [i, i, dp, dp, dp, dp, dp, dp, bp, dp, d, d, i, i,
                                       C.POINTER(d), C.POINTER(i)]
         L.orc_sor_generic.restype = i
+        L.orc_set_sor_form.argtypes = [i]
         _lib = L
     return _lib
 
@@ -100,6 +101,12 @@ def intercept(axis, direction, xF, yF, a, b, xb, yb):
 
 def target_dir(uB, uN, dF, dN):
     return lib().orc_target_dir(uB, uN, dF, dN)
+
+
+def set_sor_form(plain: bool) -> None:
+    """Selects the SOR node-update form for the whole process: False = the
+    arithmetic contract R13 (default), True = the plain IEEE form (pin only)."""
+    lib().orc_set_sor_form(1 if plain else 0)
 
 
 def sor_generic(aP, aE, aW, aN, aS, b, upd, x0, omega, tol, maxit, check_every=1):

@@ -594,13 +594,12 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
           CK(cudaEventRecord(c.tev[2 * tune_launched + 1], c.stream));
           if (++tune_launched == tune_n) tune_k_end = k + c.wf_m - 1;
         }
-        if (mult) {
-          if (!c.loopback)
-            NK(ncclAllReduce(c.rho_bits + k, c.rho_bits + k, c.wf_m, ncclUint64, ncclMax, (ncclComm_t)c.nccl,
-                             c.stream));
-          launch_sor_check(c.ctl, c.rho_bits, k, maxit, cfg.check_every, tol, c.stream, c.wf_m, 1);
-          ++c.launches;
-        }
+        if (mult && !c.loopback)
+          NK(ncclAllReduce(c.rho_bits + k, c.rho_bits + k, c.wf_m, ncclUint64, ncclMax, (ncclComm_t)c.nccl,
+                           c.stream));
+        // the decision of every fused pass (single slab too): first of its m iterations that may stop
+        launch_sor_check(c.ctl, c.rho_bits, k, maxit, cfg.check_every, tol, c.stream, c.wf_m, wf_approx() ? 1 : 0);
+        ++c.launches;
         passes.push_back({k, c.wf_m, cur});
         k += c.wf_m;
       } else {
@@ -755,6 +754,8 @@ int step_once(Ctx &c, ibm_step_stats *st) {
   // a7 projection
   CK(cudaMemsetAsync(c.nanflag, 0, sizeof(int), c.stream));
   for (Slab &s : c.sl) c.launches += launch_correct(c, s, s.us[ures], s.vs[ures], s.phi[c.phi_cur]);
+  if (c.body.has)
+    for (Slab &s : c.sl) c.launches += launch_pext(c, s, s.phi[c.phi_cur]);
   CK(cudaEventRecord(c.ev[5], c.stream));
   // history rotation
   for (Slab &s : c.sl) {
@@ -861,6 +862,12 @@ int ibm_init(const ibm_config *cfg, void *d_workspace, size_t bytes, void *cuda_
   // Automatic choice (sor_fuse = 0): m = 3 where the grid gives the fused pass
   // enough work items, else the one-iteration pass (wf_viable).
   c.wf_m = cfg->sor_fuse == 0 ? 3 : cfg->sor_fuse;
+  // (the device first: wf_viable sizes the work-item target by its SM count)
+  if (cudaSetDevice(c.device) != cudaSuccess) {
+    fprintf(stderr, "ibm_init: cudaSetDevice failed\n");
+    delete cp;
+    return IBM_ERR_CUDA;
+  }
   for (int r = 0; r < cfg->nranks; ++r) {
     int j0 = 0, j1 = cfg->ny;
     if (cfg->nranks > 1) slab_rows(cfg->ny, cfg->nranks, r, &j0, &j1);
@@ -871,12 +878,24 @@ int ibm_init(const ibm_config *cfg, void *d_workspace, size_t bytes, void *cuda_
     for (int r = 0; r < cfg->nranks; ++r) c.sl.push_back(make_slab(*cfg, r));
   else
     c.sl.push_back(make_slab(*cfg, cfg->rank));
+  // every resource created below is released on any later failure
+  for (auto &e : c.ev) e = nullptr;
+  for (auto &e : c.tev) e = nullptr;
+  c.h_ctl = nullptr;
+  c.h_red = nullptr;
+  c.h_nan = nullptr;
   auto fail = [&](int code) {
     fprintf(stderr, "ibm_init: %s\n", c.err.c_str());
+    for (auto &e : c.ev)
+      if (e) cudaEventDestroy(e);
+    for (auto &e : c.tev)
+      if (e) cudaEventDestroy(e);
+    if (c.h_ctl) cudaFreeHost(c.h_ctl);
+    if (c.h_red) cudaFreeHost(c.h_red);
+    if (c.h_nan) cudaFreeHost(c.h_nan);
     delete cp;
     return code;
   };
-  if (cudaSetDevice(c.device) != cudaSuccess) { c.err = "cudaSetDevice failed"; return fail(IBM_ERR_CUDA); }
   const size_t need = carve(c, nullptr);
   if (!d_workspace || bytes < need || ((uintptr_t)d_workspace & 255)) {
     c.err = "workspace NULL, misaligned or too small (need " + std::to_string(need) + " B)";
@@ -1114,6 +1133,16 @@ int ibm_poisson_iterate(ibm_ctx *ctx, int iters, double *rho_out) {
   c.phi_cur = pbuf;
   if (rho_out) *rho_out = rho;
   return sst == 3 ? IBM_ERR_DIVERGED : IBM_OK;
+}
+
+int ibm_query(const ibm_ctx *ctx, int key, int *out) {
+  if (!ctx || !out) return IBM_ERR_ARG;
+  switch (key) {
+    case IBM_QUERY_WF_M: *out = ctx->wf_m; return IBM_OK;
+    case IBM_QUERY_WF_L: *out = ctx->wf_L; return IBM_OK;
+    case IBM_QUERY_SLABS: *out = (int)ctx->sl.size(); return IBM_OK;
+  }
+  return IBM_ERR_ARG;
 }
 
 const char *ibm_last_error(const ibm_ctx *ctx) {

@@ -173,7 +173,9 @@ constexpr int kSorBoxW = 64, kSorBoxHx = 20, kSorBoxHb = 18;
 constexpr int kSorTileX = 60, kSorTileY = 16;
 void launch_sor_iteration(const SorArgs &a, cudaStream_t st, int grid);
 // temporally blocked Poisson pass: rows of the TMA box, segment length, launch
+int wf_cpl();  // columns per lane of the fused pass: 2 (64-column strips) or 4 (128)
 int wf_box_rows(int m);
+bool wf_approx();  // the fused pass reports high-word residual bounds (stops are provisional)
 int wf_box_cols();
 void wf_plan(WfArgs &a, int m, int L_force = 0);
 // segment lengths worth trying for this slab (the static choice first)
@@ -185,6 +187,8 @@ void launch_sor_check(SorCtl *ctl, const unsigned long long *rho_bits, int k, in
 int launch_outlet_fill(const Ctx &c, const Slab &s, double *us, const double *vs);
 int launch_prhs(const Ctx &c, const Slab &s, const double *us, const double *vs, double *phi_start);
 int launch_correct(const Ctx &c, const Slab &s, const double *us, const double *vs, const double *phi);
+// R17b pressure extension into the inactive cells next to active ones (after launch_correct)
+int launch_pext(const Ctx &c, const Slab &s, const double *phi);
 int launch_forces(const Ctx &c, const Slab &s);
 void launch_fill(double *p, const Geo &g, double val, cudaStream_t st);
 

@@ -172,8 +172,8 @@ struct PredArgs {
 };
 
 // u family: convection, AB2 (R8), grad p^n, explicit half of CN
-// (S:245), Helmholtz rhs at Fluid nodes; targets and f at Forcing nodes (R19);
-// body velocity at Solid nodes.
+// (S:245), Helmholtz rhs at Fluid nodes; targets at Forcing nodes, the body
+// velocity at Solid nodes, and the momentum forcing f at both (R19, R19b).
 __global__ void k_pred_u(PredArgs A) {
   const Geo &g = A.gu;
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -190,13 +190,6 @@ __global__ void k_pred_u(PredArgs A) {
   }
   const bool inbox = A.bu.contains(i, jl);
   const uint8_t t = inbox ? A.tu[o] : (uint8_t)FLUID;
-  if (t == SOLID) {
-    A.us[o] = 0.0;
-    A.cu[o] = 0.0;
-    A.ru[o] = 0.0;
-    A.fu[o] = 0.0;
-    return;
-  }
   const Geo &gv = A.gv, &gp = A.gp;
   const double *u = A.u, *v = A.v;
   const double uC = ld(u, g, i, jl);
@@ -232,8 +225,8 @@ __global__ void k_pred_u(PredArgs A) {
     A.ru[o] = uC + A.dt * ((-(1.5 * C - 0.5 * Cp) - Gf) + A.halfnu * L);
     A.us[o] = uC;
     if (inbox) A.fu[o] = 0.0;
-  } else {  // FORCING
-    double tgt = forcing_target(u, A.tu, g, A.bu, i, jl, A.m.xn, A.m.yc, A.B, 0.0);
+  } else {  // R19b: Forcing -> target, Solid -> body velocity; f recorded at both
+    double tgt = (t == FORCING) ? forcing_target(u, A.tu, g, A.bu, i, jl, A.m.xn, A.m.yc, A.B, 0.0) : 0.0;
     double uhat = uC + A.dt * ((-(1.5 * C - 0.5 * Cp) - G) + A.nu * L);
     A.us[o] = tgt;
     A.fu[o] = pdiv(tgt - uhat, A.dt);
@@ -257,13 +250,6 @@ __global__ void k_pred_v(PredArgs A) {
   }
   const bool inbox = A.bv.contains(i, jl);
   const uint8_t t = inbox ? A.tv[o] : (uint8_t)FLUID;
-  if (t == SOLID) {
-    A.vs[o] = A.B.vb;
-    A.cv[o] = 0.0;
-    A.rv[o] = 0.0;
-    A.fv[o] = 0.0;
-    return;
-  }
   const Geo &gu = A.gu, &gp = A.gp;
   const double *u = A.u, *v = A.v;
   const double vC = ld(v, g, i, jl);
@@ -292,8 +278,8 @@ __global__ void k_pred_v(PredArgs A) {
     A.rv[o] = vC + A.dt * ((-(1.5 * C - 0.5 * Cp) - Gf) + A.halfnu * L);
     A.vs[o] = vC;
     if (inbox) A.fv[o] = 0.0;
-  } else {
-    double tgt = forcing_target(v, A.tv, g, A.bv, i, jl, A.m.xc, A.m.yn, A.B, A.B.vb);
+  } else {  // R19b
+    double tgt = (t == FORCING) ? forcing_target(v, A.tv, g, A.bv, i, jl, A.m.xc, A.m.yn, A.B, A.B.vb) : A.B.vb;
     double vhat = vC + A.dt * ((-(1.5 * C - 0.5 * Cp) - G) + A.nu * L);
     A.vs[o] = tgt;
     A.fv[o] = pdiv(tgt - vhat, A.dt);
@@ -396,8 +382,38 @@ __global__ void k_correct_p(double *__restrict__ p, const double *__restrict__ p
   if (!isfinite(val)) atomicOr(nanflag, 1);
 }
 
-// ---------------------------------------------------------------- a8: forces (R20)
-// red[0] = sum_Forcing f_u dV, red[1] = sum_{Solid,Forcing} u dV, red[2], red[3] for v.
+// ---------------------------------------------------------------- R17b: pressure extension
+// An inactive cell with at least one active 4-neighbour takes the mean of their
+// p^{n+1} (E, W, N, S order, left fold from 0.0); deeper inactive cells keep p.
+// Runs after k_correct_p.  A neighbour in a ghost row (another slab) still holds
+// p^n there (exchanged at the start of the step), so its p^{n+1} = p^n + phi is
+// formed here -- the same IEEE addition its own slab performed.
+__global__ void k_pext(double *__restrict__ p, const double *__restrict__ phi, const uint8_t *__restrict__ pf,
+                       Geo gp, BBox pbox, int nx, int ny) {
+  const int i = pbox.i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  const int jl = max(pbox.j0, 0) + blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= pbox.i1 || jl >= min(pbox.j1, gp.nj)) return;
+  if (!(pf[gp.off(i, jl)] & PF_INACTIVE)) return;
+  double sum = 0.0;
+  int cnt = 0;
+#pragma unroll
+  for (int d = 0; d < 4; ++d) {
+    const int di = (d == 0) ? 1 : (d == 1) ? -1 : 0;
+    const int dj = (d == 2) ? 1 : (d == 3) ? -1 : 0;
+    const int in_ = i + di, jn = jl + dj, gjn = gp.gj0 + jn;
+    if (in_ < 0 || in_ >= nx || gjn < 0 || gjn >= ny) continue;
+    const uint8_t fn = pbox.contains(in_, jn) ? pf[gp.off(in_, jn)] : (uint8_t)0;
+    if (fn & PF_INACTIVE) continue;
+    const long o = gp.off(in_, jn);
+    const double pn = (jn >= 0 && jn < gp.nj) ? p[o] : p[o] + phi[o];
+    sum = sum + pn;
+    cnt = cnt + 1;
+  }
+  if (cnt > 0) p[gp.off(i, jl)] = pdiv(sum, (double)cnt);
+}
+
+// ---------------------------------------------------------------- a8: forces (R20, R19b)
+// red[0] = sum_{Solid,Forcing} f_u dV, red[1] = sum_{Solid,Forcing} u dV, red[2], red[3] for v.
 // One CTA over the body boxes: fixed reduction order (deterministic).
 __global__ void __launch_bounds__(512) k_forces(const double *__restrict__ u, const double *__restrict__ v,
                                                 const double *__restrict__ fu, const double *__restrict__ fv,
@@ -416,7 +432,7 @@ __global__ void __launch_bounds__(512) k_forces(const double *__restrict__ u, co
       if (t == FLUID) continue;
       const double dV = m.hxc[i] * m.dy[gu.gj0 + jl];
       s1 = s1 + u[o] * dV;
-      if (t == FORCING) s0 = s0 + fu[o] * dV;
+      s0 = s0 + fu[o] * dV;
     }
   }
   {
@@ -430,7 +446,7 @@ __global__ void __launch_bounds__(512) k_forces(const double *__restrict__ u, co
       if (t == FLUID) continue;
       const double dV = m.dx[i] * m.hyc[gj];
       s3 = s3 + v[o] * dV;
-      if (t == FORCING) s2 = s2 + fv[o] * dV;
+      s2 = s2 + fv[o] * dV;
     }
   }
   sh[0][threadIdx.x] = s0;
@@ -521,6 +537,15 @@ int launch_prhs(const Ctx &c, const Slab &s, const double *us, const double *vs,
   dim3 blk(128, 2);
   k_prhs<<<grid2(s.gp.ni, s.gp.nj, blk), blk, 0, c.stream>>>(us, vs, s.bp, s.q, phi_start, s.pf, s.gp, s.gu, s.gv,
                                                              s.bpb, c.m, c.nx, c.ny, c.cfg.dt);
+  return 1;
+}
+
+int launch_pext(const Ctx &c, const Slab &s, const double *phi) {
+  const BBox &b = s.bpb;
+  const int j0 = b.j0 > 0 ? b.j0 : 0, j1 = b.j1 < s.gp.nj ? b.j1 : s.gp.nj;
+  if (b.empty() || j1 <= j0) return 0;
+  dim3 blk(32, 8);
+  k_pext<<<grid2(b.i1 - b.i0, j1 - j0, blk), blk, 0, c.stream>>>(s.p, phi, s.pf, s.gp, b, c.nx, c.ny);
   return 1;
 }
 

@@ -54,21 +54,30 @@ constexpr unsigned FULL = 0xffffffffu;
 #endif
 constexpr int WNW = WF_NW;  // warps per CTA (independent work items)
 constexpr int WNT = 32 * WNW;
-// TMA stages per warp (double buffering: with 8 resident warps per SM one chunk
-// of lead keeps ~64 KB per SM in flight, measured as fast as three stages)
+// TMA prefetch distance (chunks in flight ahead of the one being computed) and
+// stages per warp.  A stage is refilled only after the chunk that follows its
+// own has been computed: the last row's b of a chunk is loaded from shared
+// memory in that chunk but first used at the start of the next one, so the
+// generic-proxy reads of the stage have all returned their values (been
+// consumed) before the async-proxy (TMA) write is issued -- no cross-proxy
+// write-after-read race, without a proxy fence.  Hence one stage more than the
+// prefetch distance.
+#ifndef WF_PD
+#define WF_PD 2
+#endif
+constexpr int WPD = WF_PD;
 template <int WM>
 __host__ __device__ constexpr int wf_nstg() {
-#ifdef WF_NSTG
-  return WF_NSTG;
-#else
-  return 2;
-#endif
+  return WPD + 1;
 }
 #ifndef WF_NS
 #define WF_NS 1
 #endif
 constexpr int NS = WF_NS;   // column pairs per lane: lane l holds pairs l + 32 st
 constexpr int SC = 64 * NS;  // stored columns per strip
+#ifndef WF_CPL_DEFAULT
+#define WF_CPL_DEFAULT 2  // columns per lane of the fused pass (wf_cpl)
+#endif
 
 template <int WM>
 struct __align__(128) WfStage {
@@ -187,7 +196,9 @@ __device__ __forceinline__ void wf_slow(double2 (&X)[NS][W], const double2 (&B)[
     const int gi = i0 + 2 * (l + 32 * st) + E;
     bool u = gi >= A.ui0 && gi < A.ui1 && gj >= A.uj0 && gj < A.uj1;
     uint8_t fl = 0;
-    if (hasf && u) fl = A.flag[A.g.off(gi, r)];
+    // rows past the stored ghost rows are never read: the cells there are junk
+    // recomputation (never stored nor counted), treated as flag 0
+    if (hasf && u && r >= -kGhost && r < A.g.nj + kGhost) fl = A.flag[A.g.off(gi, r)];
     u = u && !(fl & PF_INACTIVE);
     double aE = C.aE[st][E], aW = C.aW[st][E], aN = cN, aS = cS, aP;
     if (fl) {
@@ -335,7 +346,7 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
     if (l == 0) {
       for (int s = 0; s < NSTG; ++s) mbar_init(&bar[s], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      for (int c = 0; c < NSTG && c < nch; ++c) {
+      for (int c = 0; c < WPD && c < nch; ++c) {
         mbar_expect_tx(&bar[c], kBytes);
         tma_load_2d(&st[c].x[0][0], &A.tmx, i0, rs + c * W + kGhost, &bar[c]);
         tma_load_2d(&st[c].b[0][0], &A.tmb, i0, rs + c * W + kGhost, &bar[c]);
@@ -346,7 +357,7 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
     // TMA issue so that the control-word round trip does not delay the item's
     // first chunk; the loads in flight are waited for before leaving.
     if (*(volatile int *)&A.ctl->k_done >= 0) {
-      for (int c = 0; c < NSTG && c < nch; ++c) mbar_wait_warp(&bar[c], 0);
+      for (int c = 0; c < WPD && c < nch; ++c) mbar_wait_warp(&bar[c], 0);
       return;
     }
     bool lane_own[NS];
@@ -416,13 +427,13 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
       else
         wf_chunk<WM, TP, 0, false, APX>(X, B, st[s], C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax);
       __syncwarp();
-      if (l == 0 && c + NSTG < nch) {
-        // (no proxy fence: the stage's generic reads were all consumed by this
-        // warp's arithmetic before the __syncwarp above, so the TMA write cannot
-        // overtake them; a fence here is a MEMBAR that also drains the stores)
-        mbar_expect_tx(&bar[s], kBytes);
-        tma_load_2d(&st[s].x[0][0], &A.tmx, i0, rs + (c + NSTG) * W + kGhost, &bar[s]);
-        tma_load_2d(&st[s].b[0][0], &A.tmb, i0, rs + (c + NSTG) * W + kGhost, &bar[s]);
+      if (l == 0 && c + WPD < nch) {
+        // refill the stage of chunk c - 1 (see wf_nstg): every lane consumed the
+        // values it read from it before the __syncwarp above
+        const int sr = (c + WPD) % NSTG;
+        mbar_expect_tx(&bar[sr], kBytes);
+        tma_load_2d(&st[sr].x[0][0], &A.tmx, i0, rs + (c + WPD) * W + kGhost, &bar[sr]);
+        tma_load_2d(&st[sr].b[0][0], &A.tmb, i0, rs + (c + WPD) * W + kGhost, &bar[sr]);
       }
     }
   }
@@ -449,29 +460,335 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
       for (int v = 0; v < WNW; ++v) mx = umax64(mx, wmax[v][i]);
       if (mx) atomicMax(&A.rho_bits[A.k + i], mx);
     }
-    if (A.multi) return;  // decided by k_sor_check after the cross-slab reduction
-    __threadfence();
-    const unsigned tk = atomicAdd(&A.ctl->ticket, 1u);
-    if (tk == gridDim.x - 1) {
-      A.ctl->ticket = 0;
-      // first of the WM iterations that stops the solve (same test as sor_decide;
-      // APX: on the lower bound LB <= rho, so every true stop is caught and marked
-      // provisional (status 4) -- as is LB = +Inf, which may hide a NaN)
-      for (int i = 0; i < WM; ++i) {
-        const int k = A.k + i;
-        const unsigned long long rb = atomicAdd(&A.rho_bits[k], 0ull);
-        const double rho = __longlong_as_double((long long)rb);
-        const bool nan_ = isnan(rho) || (APX && (rb >> 32) == 0x7ff00000ull);
-        const bool conv = (k % A.check_every == 0) && rho <= A.tol;
-        if (nan_ || conv || k >= A.maxit) {
-          A.ctl->rho_final = rb;
-          A.ctl->status = APX ? 4 : (nan_ ? 3 : (conv ? 0 : 1));
-          __threadfence();
-          A.ctl->k_done = k;
-          break;
-        }
-      }
+    // The stop decision is taken by k_sor_check, launched after the pass (after the
+    // cross-slab reduction on decomposed grids): deciding in the pass's last CTA
+    // needs a __threadfence per CTA, which waits for the CTA's outstanding stores
+    // (ncu: ~5 % of the pass's stall samples at 8192^2).
+  }
+}
+
+// ============================================================================
+// Four contiguous columns per lane (CPL = 4): lane l holds the column pairs
+// (4l, 4l+1) and (4l+2, 4l+3) of a 128-column strip (128 - 4WM owned instead of
+// 64 - 4WM), so one half-sweep of a row needs one shuffle per two node updates
+// (the pair at the lane's other end reads its neighbour from the lane itself)
+// and the warp carries two independent updates per row and half-sweep.  The
+// register window is the same W = 2WM+2 rows; it arrives by TMA in two halves of
+// WM+1 rows (8 KB per half at WM = 3) so that three stages still fit eight warps
+// per SM.  Arithmetic, colours and the order of every update are those of the
+// CPL = 2 kernel above (and of the oracle): same FMA chain, same reciprocal.
+constexpr int SC4 = 128;  // stored columns per strip
+template <int WM>
+struct __align__(128) Wf4Stage {
+  double x[WM + 1][SC4];
+  double b[WM + 1][SC4];
+};
+template <int WM>
+constexpr size_t wf4_smem() {
+  return (size_t)(WPD + 1) * (sizeof(Wf4Stage<WM>) + sizeof(unsigned long long));
+}
+template <int WM>
+constexpr int wf4_min_blocks() {
+  return (int)((220u * 1024u) / wf4_smem<WM>()) < 8 ? (int)((220u * 1024u) / wf4_smem<WM>()) : 8;
+}
+
+struct Wf4Cols {  // [pair st][element e] of the lane's columns gi = i0 + 4l + 2st + e
+  double aE[2][2], aW[2][2], yu[2][2];
+  unsigned inm[2][2];
+};
+
+// the four (W, E) neighbours of the two pairs' element E in window slot Q
+template <int W, int Q, int E>
+__device__ __forceinline__ void wf4_nb(const double2 (&X)[W][2], double (&xw)[2], double (&xe)[2]) {
+  const int l = threadIdx.x & 31;
+  if (E == 0) {  // columns 4l, 4l+2: west of 4l is lane l-1's column 4l-1
+    xw[0] = __shfl_sync(FULL, X[Q][1].y, (l + 31) & 31);
+    xe[0] = X[Q][0].y;
+    xw[1] = X[Q][0].y;
+    xe[1] = X[Q][1].y;
+  } else {  // columns 4l+1, 4l+3: east of 4l+3 is lane l+1's column 4l+4
+    xw[0] = X[Q][0].x;
+    xe[0] = X[Q][1].x;
+    xw[1] = X[Q][1].x;
+    xe[1] = __shfl_sync(FULL, X[Q][0].x, (l + 1) & 31);
+  }
+}
+
+template <int W, int Q, int E, bool EDGE, bool APX>
+__device__ __forceinline__ void wf4_fast(double2 (&X)[W][2], const double2 (&B)[W][2], const Wf4Cols &C, double aN,
+                                         double aS, double omega, unsigned okm, unsigned long long (&tmax)[2]) {
+  constexpr int QN = (Q + 1) % W, QS = (Q + W - 1) % W;
+  double xw[2], xe[2];
+  wf4_nb<W, Q, E>(X, xw, xe);
+#pragma unroll
+  for (int st = 0; st < 2; ++st) {
+    const double xo = rd(X[Q][st], E), xN = rd(X[QN][st], E), xS = rd(X[QS][st], E);
+    const double nm = __fma_rn(aN, xN, __fma_rn(C.aE[st][E], xe[st], __fma_rn(C.aW[st][E], xw[st],
+                                                                               __fma_rn(aS, xS, rd(B[Q][st], E)))));
+    const double d = __fma_rn(nm, C.yu[st][E], -xo);  // gs - x_old, one rounding (R13)
+    const double xn = __fma_rn(omega, d, xo);
+    wr(X[Q][st], E, (!EDGE || C.inm[st][E]) ? xn : xo);
+    wf_acc<APX>(tmax[st], d, EDGE ? (okm & C.inm[st][E]) : okm);
+  }
+}
+
+template <int W, int Q, int E, bool APX>
+__device__ __forceinline__ void wf4_slow(double2 (&X)[W][2], const double2 (&B)[W][2], const Wf4Cols &C,
+                                         const WfArgs &A, int r, int i0, bool hasf, double omega, bool own,
+                                         unsigned long long (&tmax)[2]) {
+  constexpr int QN = (Q + 1) % W, QS = (Q + W - 1) % W;
+  const int l = threadIdx.x & 31;
+  const int gj = A.g.gj0 + r;
+  double cN = 0.0, cS = 0.0;  // 0 outside the family (oracle: out-of-range coefficient)
+  if (gj >= 0 && gj < A.g.NJ) {
+    cN = A.cN[gj];
+    cS = A.cS[gj];
+  }
+  double xw[2], xe[2];
+  wf4_nb<W, Q, E>(X, xw, xe);
+#pragma unroll
+  for (int st = 0; st < 2; ++st) {
+    const int gi = i0 + 4 * l + 2 * st + E;
+    const bool in = gi >= 0 && gi < A.g.ni;
+    bool u = gi >= A.ui0 && gi < A.ui1 && gj >= A.uj0 && gj < A.uj1;
+    uint8_t fl = 0;
+    // rows past the stored ghost rows are junk recomputation (never stored nor counted)
+    if (hasf && u && r >= -kGhost && r < A.g.nj + kGhost) fl = A.flag[A.g.off(gi, r)];
+    u = u && !(fl & PF_INACTIVE);
+    const double cD = in ? __ldg(A.cD + gi) : 0.0;
+    double aE = C.aE[st][E], aW = C.aW[st][E], aN = cN, aS = cS, aP;
+    if (fl) {
+      aE = (fl & PF_E) ? 0.0 : aE;
+      aW = (fl & PF_W) ? 0.0 : aW;
+      aN = (fl & PF_N) ? 0.0 : aN;
+      aS = (fl & PF_S) ? 0.0 : aS;
+      aP = ((aE + aW) + (aN + aS)) + cD;
+    } else {
+      aP = ((aE + aW) + (cN + cS)) + cD;
     }
+    const double xo = rd(X[Q][st], E), xN = rd(X[QN][st], E), xS = rd(X[QS][st], E);
+    const double nm = __fma_rn(aN, xN, __fma_rn(aE, xe[st], __fma_rn(aW, xw[st], __fma_rn(aS, xS, rd(B[Q][st], E)))));
+    const double d = __fma_rn(nm, __drcp_rn(aP), -xo);
+    if (u) {
+      wr(X[Q][st], E, __fma_rn(omega, d, xo));
+      if (own) wf_acc<APX>(tmax[st], d, 0xffffffffu);
+    }
+  }
+}
+
+// One half (HALF = 0: slots 0..WM, 1: slots WM+1..2WM+1) of the window of W rows
+// rb .. rb+W-1; its rows come from stage S.
+template <int WM, int TP, int MODE, bool OWN, bool APX, int HALF>
+__device__ __forceinline__ void wf4_half(double2 (&X)[2 * WM + 2][2], double2 (&B)[2 * WM + 2][2],
+                                         const Wf4Stage<WM> &S, const Wf4Stage<WM> &Sp, const Wf4Cols &C,
+                                         const WfArgs &A, int rb, int j0,
+                                         int j1, int i0, const bool (&lane_own)[2], bool hasf, double cN0, double cS0,
+                                         unsigned long long (&tmax)[WM][2]) {
+  constexpr int W = 2 * WM + 2, CR = WM + 1;
+  const int l = threadIdx.x & 31;
+  const double omega = A.omega;
+  const long pitch = A.g.pitch;
+  double *const ob = A.xout + (long)(rb - 2 * WM + kGhost) * pitch + (i0 + 4 * l);
+  sfor<CR>([&](auto qc) {
+    constexpr int qq = decltype(qc)::value;
+    constexpr int q = HALF * CR + qq;  // window slot = row rb + q
+    // row rb+q enters the window; b of row rb+q-1 (first needed now) is read now,
+    // not with its x, which shortens its live range by one row (registers)
+    constexpr int qb = (q + W - 1) % W;
+#pragma unroll
+    for (int st = 0; st < 2; ++st) {
+      X[q][st] = *reinterpret_cast<const double2 *>(&S.x[qq][4 * l + 2 * st]);
+      B[qb][st] = *reinterpret_cast<const double2 *>(qq == 0 ? &Sp.b[CR - 1][4 * l + 2 * st]
+                                                              : &S.b[qq == 0 ? 0 : qq - 1][4 * l + 2 * st]);
+    }
+    sfor<2 * WM>([&](auto hc) {
+      constexpr int h = decltype(hc)::value;
+      constexpr int Q = ((q - 1 - h) % W + W) % W;  // slot of row rb + q - 1 - h
+      constexpr int E = (TP + Q + h) & 1;           // red (h even): (i + j) even
+      const int r = rb + q - 1 - h;
+      [[maybe_unused]] const bool own = OWN || (r >= j0 && r < j1);
+      unsigned okm = 0xffffffffu;
+      if (!OWN)
+        asm("{\n .reg .b32 t;\n or.b32 t, %1, %2;\n shr.s32 t, t, 31;\n not.b32 %0, t;\n}"
+            : "=r"(okm)
+            : "r"(r - j0), "r"(j1 - 1 - r));
+      if constexpr (MODE > 0)
+        wf4_fast<W, Q, E, MODE == 1, APX>(X, B, C, cN0, cS0, omega, okm, tmax[h / 2]);
+      else
+        wf4_slow<W, Q, E, APX>(X, B, C, A, r, i0, hasf, omega, own, tmax[h / 2]);
+    });
+    const int ro = rb + q - 2 * WM;  // row that has received its last half-sweep
+    const bool rowin = OWN || (ro >= j0 && ro < j1);
+#pragma unroll
+    for (int st = 0; st < 2; ++st) {
+      const double2 v = X[((q - 2 * WM) % W + W) % W][st];
+      const bool pair_in = MODE == 2 || i0 + 4 * l + 2 * st + 1 < A.g.ni;
+      st_pred(rowin && lane_own[st] && pair_in, ob + q * pitch + 2 * st, v);
+      if (MODE < 2) st_pred1(rowin && lane_own[st] && !pair_in, ob + q * pitch + 2 * st, v.x);
+    }
+  });
+}
+
+template <int WM, int TP, int MODE, bool OWN, bool APX>
+__device__ __forceinline__ void wf4_window(double2 (&X)[2 * WM + 2][2], double2 (&B)[2 * WM + 2][2],
+                                           Wf4Stage<WM> *st, unsigned long long *bar, const Wf4Cols &C,
+                                           const WfArgs &A, int c, int nhc, int rs, int rb, int j0, int j1, int i0,
+                                           const bool (&lane_own)[2], bool hasf, double cN0, double cS0,
+                                           unsigned long long (&tmax)[WM][2]) {
+  constexpr int NSTG = WPD + 1, CR = WM + 1;
+  constexpr unsigned kHalf = 2u * CR * SC4 * 8;
+  const int l = threadIdx.x & 31;
+  auto refill = [&](int hc) {
+    __syncwarp();
+    if (l == 0 && hc + WPD < nhc) {
+      // stage of half-window hc - 1: every lane consumed its values before the __syncwarp
+      const int h2 = hc + WPD, sr = h2 % NSTG;
+      mbar_expect_tx(&bar[sr], kHalf);
+      tma_load_2d(&st[sr].x[0][0], &A.tmx, i0, rs + h2 * CR + kGhost, &bar[sr]);
+      tma_load_2d(&st[sr].b[0][0], &A.tmb, i0, rs + h2 * CR + kGhost, &bar[sr]);
+    }
+  };
+  // (the first window's "previous" stage is its own: the b it supplies there
+  // belongs to row rs-1, a junk row never stored nor counted)
+  const int h0 = 2 * c, h1 = 2 * c + 1, hp = c > 0 ? h0 - 1 : h0;
+  mbar_wait_warp(&bar[h0 % NSTG], (h0 / NSTG) & 1);
+  wf4_half<WM, TP, MODE, OWN, APX, 0>(X, B, st[h0 % NSTG], st[hp % NSTG], C, A, rb, j0, j1, i0, lane_own, hasf, cN0,
+                                      cS0, tmax);
+  refill(h0);
+  mbar_wait_warp(&bar[h1 % NSTG], (h1 / NSTG) & 1);
+  wf4_half<WM, TP, MODE, OWN, APX, 1>(X, B, st[h1 % NSTG], st[h0 % NSTG], C, A, rb, j0, j1, i0, lane_own, hasf, cN0,
+                                      cS0, tmax);
+  refill(h1);
+}
+
+template <int WM, int TP, bool APX>
+__global__ void __launch_bounds__(32, wf4_min_blocks<WM>()) k_sor_wf4(const __grid_constant__ WfArgs A) {
+  constexpr int W = 2 * WM + 2, OW = SC4 - 4 * WM, NSTG = WPD + 1, CR = WM + 1;
+  constexpr unsigned kHalf = 2u * CR * SC4 * 8;
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  const int l = threadIdx.x & 31;
+  Wf4Stage<WM> *st = reinterpret_cast<Wf4Stage<WM> *>(smraw);
+  unsigned long long *bar = reinterpret_cast<unsigned long long *>(smraw + (size_t)NSTG * sizeof(Wf4Stage<WM>));
+  unsigned long long tmax[WM][2];
+#pragma unroll
+  for (int i = 0; i < WM; ++i) tmax[i][0] = tmax[i][1] = 0ull;
+  const int item = blockIdx.x;
+  const Geo &g = A.g;
+  int sx = item / A.segs, sy = item % A.segs;  // strip-major item order
+  if (A.order == 0) {
+    sx = item % A.strips;
+    sy = item / A.strips;
+  }
+  const int i0 = sx * OW - 2 * WM;  // global column of stored column 0
+  const int j0 = sy * A.L;          // owned local rows [j0, j1)
+  const int j1 = min(j0 + A.L, g.nj);
+  const int rs = j0 - 2 * WM;       // first streamed row
+  const int nwin = ((j1 - j0) + 4 * WM + W - 1) / W;
+  const int nhc = 2 * nwin;
+  if (l == 0) {
+    for (int s = 0; s < NSTG; ++s) mbar_init(&bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int h = 0; h < WPD && h < nhc; ++h) {
+      mbar_expect_tx(&bar[h], kHalf);
+      tma_load_2d(&st[h].x[0][0], &A.tmx, i0, rs + h * CR + kGhost, &bar[h]);
+      tma_load_2d(&st[h].b[0][0], &A.tmb, i0, rs + h * CR + kGhost, &bar[h]);
+    }
+  }
+  __syncwarp();
+  if (*(volatile int *)&A.ctl->k_done >= 0) {  // converged at an earlier iteration
+    for (int h = 0; h < WPD && h < nhc; ++h) mbar_wait_warp(&bar[h], 0);
+    return;
+  }
+  bool lane_own[2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const int p = 2 * l + s;  // pair index in the strip
+    lane_own[s] = p >= WM && p <= SC4 / 2 - 1 - WM && i0 + 2 * p < g.ni;
+  }
+  const bool interior = i0 >= A.ui0 && i0 + SC4 <= A.ui1;
+  const bool boxstrip = !A.box.empty() && i0 < A.box.i1 && i0 + SC4 > A.box.i0;
+  const int jr = min(max(g.gj0 + j0 + A.L / 2, 1), g.NJ - 2);
+  const double cN0 = A.cN[jr], cS0 = A.cS[jr];
+  Wf4Cols C;
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int gi = i0 + 4 * l + 2 * s + e;
+      const bool in = gi >= 0 && gi < g.ni;
+      const double cE = in ? A.cE[gi] : 0.0, cW = in ? A.cW[gi] : 0.0, cD = in ? A.cD[gi] : 0.0;
+      C.aE[s][e] = cE;
+      C.aW[s][e] = cW;
+      C.yu[s][e] = __drcp_rn(((cE + cW) + (cN0 + cS0)) + cD);
+      C.inm[s][e] = (gi >= A.ui0 && gi < A.ui1) ? 0xffffffffu : 0u;
+    }
+  double2 X[W][2], B[W][2];
+#pragma unroll
+  for (int q = 0; q < W; ++q) X[q][0] = X[q][1] = B[q][0] = B[q][1] = make_double2(0.0, 0.0);
+  int irr0 = INT_MAX, irr1 = INT_MIN;
+#pragma unroll 4
+  for (int r = rs - 2 * WM + l; r <= rs + nwin * W - 2; r += 32) {
+    const int gj = g.gj0 + r;
+    const int gjc = min(max(gj, 0), g.NJ - 1);
+    const double cn = __ldg(A.cN + gjc), cs = __ldg(A.cS + gjc);
+    const bool reg = (gj >= A.uj0) & (gj < A.uj1) & !(boxstrip & (r >= A.box.j0) & (r < A.box.j1)) &
+                     (cn == cN0) & (cs == cS0);
+    if (!reg) {
+      irr0 = min(irr0, r);
+      irr1 = max(irr1, r);
+    }
+  }
+  irr0 = __reduce_min_sync(FULL, irr0);
+  irr1 = __reduce_max_sync(FULL, irr1);
+  for (int c = 0; c < nwin; ++c) {
+    const int rb = rs + c * W;
+    const bool fast = rb + W - 2 < irr0 || rb - 2 * WM > irr1;
+    const bool hasf = boxstrip && rb + W - 2 >= A.box.j0 && rb - 2 * WM < A.box.j1;
+    const bool ownall = rb - 2 * WM >= j0 && rb + W - 2 < j1;
+    if (fast && interior && ownall)
+      wf4_window<WM, TP, 2, true, APX>(X, B, st, bar, C, A, c, nhc, rs, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax);
+    else if (fast && interior)
+      wf4_window<WM, TP, 2, false, APX>(X, B, st, bar, C, A, c, nhc, rs, rb, j0, j1, i0, lane_own, hasf, cN0, cS0,
+                                        tmax);
+    else if (fast)
+      wf4_window<WM, TP, 1, false, APX>(X, B, st, bar, C, A, c, nhc, rs, rb, j0, j1, i0, lane_own, hasf, cN0, cS0,
+                                        tmax);
+    else
+      wf4_window<WM, TP, 0, false, APX>(X, B, st, bar, C, A, c, nhc, rs, rb, j0, j1, i0, lane_own, hasf, cN0, cS0,
+                                        tmax);
+  }
+  // residual of each fused iteration: lanes -> warp -> atomicMax on the bit pattern
+  // (halo pairs accumulated recomputed cells: dropped here); the stop decision is
+  // k_sor_check's, after the pass
+#pragma unroll
+  for (int i = 0; i < WM; ++i) {
+    unsigned long long t = 0ull;
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+      if (2 * l + s >= WM && 2 * l + s <= SC4 / 2 - 1 - WM) t = umax64(t, tmax[i][s]);
+#pragma unroll
+    for (int off = 16; off; off >>= 1) t = umax64(t, __shfl_xor_sync(FULL, t, off));
+    if (l == 0 && t) atomicMax(&A.rho_bits[A.k + i], APX ? t << 32 : t);  // APX: LB = H << 32
+  }
+}
+
+template <int WM, int TP, bool APX>
+void wf4_prepare() {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(k_sor_wf4<WM, TP, APX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wf4_smem<WM>());
+    done = true;
+  }
+}
+
+template <int WM, bool APX>
+void wf4_launch_tp(const WfArgs &a, cudaStream_t s) {
+  if (a.g.gj0 & 1) {
+    wf4_prepare<WM, 1, APX>();
+    k_sor_wf4<WM, 1, APX><<<a.items, 32, wf4_smem<WM>(), s>>>(a);
+  } else {
+    wf4_prepare<WM, 0, APX>();
+    k_sor_wf4<WM, 0, APX><<<a.items, 32, wf4_smem<WM>(), s>>>(a);
   }
 }
 
@@ -504,17 +821,36 @@ void wf_launch_tp(const WfArgs &a, cudaStream_t s) {
 template <int WM>
 cudaError_t wf_launch(const WfArgs &a, cudaStream_t s) {
 #ifdef WF_EXACT
-  wf_launch_tp<WM, false>(a, s);
+  constexpr bool kApx = false;
 #else
-  wf_launch_tp<WM, true>(a, s);
+  constexpr bool kApx = true;
 #endif
+  if (wf_cpl() == 4)
+    wf4_launch_tp<WM, kApx>(a, s);
+  else
+    wf_launch_tp<WM, kApx>(a, s);
   return cudaGetLastError();
 }
 
 }  // namespace
 
-int wf_box_rows(int m) { return 2 * m + 2; }
-int wf_box_cols() { return SC; }
+// columns per lane of the fused pass (2: 64-column strips, 4: 128-column strips),
+// fixed per process (the TMA boxes are built at init); IBM_WF_CPL overrides
+int wf_cpl() {
+  static const int cpl = [] {
+    const char *e = std::getenv("IBM_WF_CPL");
+    const int v = e ? std::atoi(e) : WF_CPL_DEFAULT;
+    return v == 4 ? 4 : 2;
+  }();
+  return cpl;
+}
+int wf_box_rows(int m) { return wf_cpl() == 4 ? m + 1 : 2 * m + 2; }
+#ifdef WF_EXACT
+bool wf_approx() { return false; }
+#else
+bool wf_approx() { return true; }
+#endif
+int wf_box_cols() { return wf_cpl() == 4 ? SC4 : SC; }
 
 // Strip / segment plan: segments of L owned rows, L = 64 for m = 2 and 256 for
 // m >= 3, halved (down to 32 / 64) while the items would not fill two waves
@@ -526,11 +862,13 @@ int wf_box_cols() { return SC; }
 // scripts/gpu_wf_rows.sh).  IBM_WF_ROWS overrides L for tuning; it is rounded up
 // to even so colours stay compile-time.
 namespace {
+// SM count of the current device (cached per device ordinal)
 int sm_count() {
-  static int sms = 0;
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int &sms = cache[dev & 63];
   if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms < 1) sms = 1;
   }
@@ -540,7 +878,10 @@ int sm_count() {
 int wf_items_target() { return 2 * 8 * sm_count(); }
 int wf_rows_default(int m) { return m == 2 ? 64 : 256; }
 int wf_rows_min(int m) { return m == 2 ? 32 : 64; }
-int wf_strips(int ni, int m) { return (ni + SC - 4 * m - 1) / (SC - 4 * m); }
+int wf_strips(int ni, int m) {
+  const int sc = wf_box_cols();
+  return (ni + sc - 4 * m - 1) / (sc - 4 * m);
+}
 }  // namespace
 
 // The fused pass needs enough work items to fill the GPU at its shortest

@@ -56,7 +56,8 @@ class ibm_step_stats(C.Structure):
 
 EXPORTS = ["ibm_workspace_size", "ibm_nccl_unique_id", "ibm_init", "ibm_set_body", "ibm_clear_body",
            "ibm_set_fields", "ibm_set_step", "ibm_step", "ibm_get_fields", "ibm_forces",
-           "ibm_poisson_iterate", "ibm_last_error", "ibm_destroy"]
+           "ibm_poisson_iterate", "ibm_query", "ibm_last_error", "ibm_destroy"]
+IBM_QUERY_WF_M, IBM_QUERY_WF_L, IBM_QUERY_SLABS = 0, 1, 2
 
 _lib = None
 
@@ -84,6 +85,7 @@ def lib():
         L.ibm_get_fields.argtypes = [vp, C.c_uint, C.POINTER(vp), i, C.POINTER(i), C.POINTER(i)]
         L.ibm_forces.argtypes = [vp, C.POINTER(d)]
         L.ibm_poisson_iterate.argtypes = [vp, i, C.POINTER(d)]
+        L.ibm_query.argtypes = [vp, i, C.POINTER(i)]
         L.ibm_last_error.argtypes = [vp]
         L.ibm_last_error.restype = C.c_char_p
         L.ibm_destroy.argtypes = [vp]
@@ -191,6 +193,12 @@ def ibm_poisson_iterate(ctx, iters):
     st = lib().ibm_poisson_iterate(ctx, iters, C.byref(rho))
     _check("ibm_poisson_iterate", st, ctx, ok=(IBM_OK, IBM_ERR_DIVERGED))
     return st, rho.value
+
+
+def ibm_query(ctx, key) -> int:
+    out = C.c_int(0)
+    _check("ibm_query", lib().ibm_query(ctx, key, C.byref(out)), ctx)
+    return out.value
 
 
 def ibm_last_error(ctx) -> str:
@@ -331,3 +339,9 @@ class Solver:
 
     def poisson_iterate(self, iters):
         return ibm_poisson_iterate(self.ctx, iters)
+
+    def query(self, key):
+        """Launch configuration chosen by the library: "wf_m" (Poisson iterations per
+        HBM pass), "wf_L" (fused-pass segment length, 0 before tuning), "slabs"."""
+        return ibm_query(self.ctx, {"wf_m": IBM_QUERY_WF_M, "wf_L": IBM_QUERY_WF_L,
+                                    "slabs": IBM_QUERY_SLABS}[key])

@@ -278,8 +278,13 @@ def test_full_size_parity_vs_oracle(mods):
         b = o.get(n)
         assert rel_l2(a, b) <= FIELD_TOL, n
         assert np.array_equal(a, b), (n, np.abs(a - b).max())
+    # one step from the impulsive start: u_hat = u^n at every body node, so the two
+    # sums of S:355 (each ~ 2 pi a b / dt ~ 2e3 here) cancel to round-off (R19b) and
+    # the coefficient is noise of that size; the relative bar is taken on that scale
+    b = cfg.body
+    term = 2.0 * math.pi * b.a * b.b / cfg.dt
     for col in (5, 6):
-        assert abs(stg[0, col] - sto[0, col]) <= FORCE_TOL * max(abs(sto[0, col]), 1e-30)
+        assert abs(stg[0, col] - sto[0, col]) <= FORCE_TOL * max(abs(sto[0, col]), term)
 
 
 def test_persistent_and_launched_sor_agree(mods):
