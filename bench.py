@@ -142,23 +142,42 @@ def oracle_sample_n(n_req, requested):
     return n
 
 
-def run_oracle_steps(n, steps, maxit_p, maxit_uv):
-    """One oracle instance on the N x N workload; each step capped at maxit
-    iterations (a bounded sample).  Returns (updates/s, seconds, stats, n)."""
+ORACLE_SAMPLE_MAXIT_P, ORACLE_SAMPLE_MAXIT_UV = 20, 5
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_oracle_steps(n, steps, maxit_p, maxit_uv, omp=False):
+    """One oracle instance (oracle_seq, or oracle_omp on every host core) on the
+    N x N workload of the bench, each step with the SOR solves capped at
+    maxit_p / maxit_uv iterations (a bounded sample).  Returns
+    (updates/s, seconds, stats, per-step list, Poisson updates/s)."""
+    if omp:
+        os.environ["OMP_NUM_THREADS"] = str(host_cores())  # read when the OpenMP runtime starts
     from oracle import oracle as O
     O.build()
     cfg = I.cfg4(n=n, maxit_p=maxit_p, maxit_uv=maxit_uv)
-    o = O.Oracle(cfg.xn, cfg.yn, **cfg.solver_kwargs())
+    o = O.Oracle(cfg.xn, cfg.yn, omp=omp, **cfg.solver_kwargs())
     o.set_body(*cfg.body_args())
     o.set_fields(*I.initial_fields(cfg.nx, cfg.ny))
+    o.timers()
     per = []
+    psec = 0.0
     for _ in range(steps):
         t0 = time.perf_counter()
         st, stats = o.step(1)
         per.append((time.perf_counter() - t0, stats))
+        psec += o.timers()[4]  # region "P solver" (Table 1 layout)
     secs = sum(p[0] for p in per)
     allstats = np.concatenate([p[1] for p in per])
-    return updates_for(allstats, cfg.nx, cfg.ny) / secs, secs, allstats, per
+    p_rate = float(allstats[:, 2].sum()) * cfg.nx * cfg.ny / max(psec, 1e-12)
+    del o
+    return updates_for(allstats, cfg.nx, cfg.ny) / secs, secs, allstats, per, p_rate
 
 
 def cpu_model():
@@ -172,11 +191,22 @@ def cpu_model():
 
 
 def cpu_baseline(args):
+    """The oracle as it stands on this host: oracle_omp on every core (the headline
+    value) and oracle_seq on one core, each for one time step of the bench's own
+    N x N workload with the SOR solves capped at 20 Poisson / 5 velocity
+    iterations (the bounded sample; the GPU runs the uncapped solve)."""
     n = oracle_sample_n(args.n, args.cpu_sample_n)
-    v, secs, stats, _ = run_oracle_steps(n, 1, 3, 3)
-    return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": "1 time step of the %dx%d foil workload with SOR capped at 3+3 iterations "
-                      "(%.1f s, single-threaded plain-C oracle, %s)" % (n, n, secs, cpu_model())}
+    mp, mu = ORACLE_SAMPLE_MAXIT_P, ORACLE_SAMPLE_MAXIT_UV
+    v1, s1, _, _, p1 = run_oracle_steps(n, 1, mp, mu, omp=False)
+    cores = host_cores()
+    vN, sN, _, _, pN = run_oracle_steps(n, 1, mp, mu, omp=True)
+    return {"value": vN, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": "1 time step of the %dx%d foil workload (BJ configs[3]) with the SOR solves capped at "
+                      "%d Poisson + %d velocity iterations; oracle_omp (same C source, -fopenmp, rows of one "
+                      "colour split over %d threads, bitwise equal to oracle_seq) %.1f s; %s"
+                      % (n, n, mp, mu, cores, sN, cpu_model()),
+            "poisson_updates_per_s": pN,
+            "seq": {"value": v1, "cores": 1, "seconds": s1, "poisson_updates_per_s": p1}}
 
 
 # ---------------------------------------------------------------- reference arm = oracle
@@ -184,9 +214,10 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     n = oracle_sample_n(args.n, args.cpu_sample_n)
-    maxit = 3
+    mp, mu = ORACLE_SAMPLE_MAXIT_P, ORACLE_SAMPLE_MAXIT_UV
     total = args.warmup + args.steps
-    v, secs, stats, per = run_oracle_steps(n, total, maxit, maxit)
+    cores = host_cores()
+    v, secs, stats, per, p_rate = run_oracle_steps(n, total, mp, mu, omp=True)
     timed = per[args.warmup:]
     tsec = sum(p[0] for p in timed)
     tstats = np.concatenate([p[1] for p in timed])
@@ -197,10 +228,12 @@ def run_reference(args, rank, world):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": "cfg4-foil-%dx%d" % (args.n, args.n), "oracle_sample_n": n,
-                       "maxit_p": maxit, "maxit_uv": maxit},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": "%d oracle time steps of the %dx%d foil workload, SOR capped at %d+%d "
-                                       "iterations per step (%s)" % (args.steps, n, n, maxit, maxit, cpu_model())},
+                       "maxit_p": mp, "maxit_uv": mu},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": "%d oracle_omp time steps of the %dx%d foil workload on %d host cores, SOR "
+                                       "capped at %d Poisson + %d velocity iterations per step (%s)"
+                                       % (args.steps, n, n, cores, mp, mu, cpu_model()),
+                             "poisson_updates_per_s": p_rate},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

@@ -169,8 +169,10 @@ IBM_API int ibm_poisson_iterate(ibm_ctx *ctx, int iters, double *rho_out);
  *   IBM_QUERY_WF_L  segment length (owned rows per work item) of the fused pass, 0
  *                   until the online tuner has chosen one
  *   IBM_QUERY_SLABS slabs held by this ctx (loopback: nranks, else 1)
+ *   IBM_QUERY_TB_M  Poisson iterations per grid barrier of the resident persistent
+ *                   solve used on mid-size single-slab grids (0 = not used)
  * IBM_ERR_ARG for an unknown key or NULL pointers.  No device work. */
-enum { IBM_QUERY_WF_M = 0, IBM_QUERY_WF_L = 1, IBM_QUERY_SLABS = 2 };
+enum { IBM_QUERY_WF_M = 0, IBM_QUERY_WF_L = 1, IBM_QUERY_SLABS = 2, IBM_QUERY_TB_M = 3 };
 IBM_API int ibm_query(const ibm_ctx *ctx, int key, int *out);
 
 /* Human-readable cause of the last error on ctx (never NULL). */

@@ -94,6 +94,16 @@ static void tick(orc_ctx *c, int r, double *t0)
     *t0 = t;
 }
 
+/* ORC_PAR: row loops whose iterations write disjoint elements (the OpenMP build,
+ * -fopenmp, splits them over threads; without it the pragma is ignored and the
+ * oracle is the plain one-thread program).  Sum reductions (forces, solid
+ * momentum) are never parallelised, so both builds are bitwise identical. */
+#ifdef _OPENMP
+#define ORC_PAR _Pragma("omp parallel for schedule(static)")
+#else
+#define ORC_PAR
+#endif
+
 static double *dalloc(size_t n) { return (double *)calloc(n ? n : 1, sizeof(double)); }
 static unsigned char *balloc(size_t n) { return (unsigned char *)calloc(n ? n : 1, 1); }
 
@@ -222,12 +232,14 @@ static void classify_family(const orc_ctx *c, int fam, double yb, unsigned char 
     int ni = fam_ni(c, fam), nj = fam_nj(c, fam);
     size_t n = (size_t)ni * (size_t)nj;
     unsigned char *in = balloc(n);
+    ORC_PAR
     for (int j = 0; j < nj; ++j)
         for (int i = 0; i < ni; ++i) {
             double x, y;
             node_xy(c, fam, i, j, &x, &y);
             in[(size_t)j * ni + i] = c->has_body ? (unsigned char)orc_inside(x, y, c->a, c->b, c->x0, yb) : 0;
         }
+    ORC_PAR
     for (int j = 0; j < nj; ++j)
         for (int i = 0; i < ni; ++i) {
             size_t id = (size_t)j * ni + i;
@@ -271,6 +283,7 @@ static void convection(const orc_ctx *c, const double *u, const double *v, doubl
     for (size_t id = 0; id < nv; ++id) cv[id] = 0.0;
 #define U(i, j) u[UI(c, i, j)]
 #define V(i, j) v[VI(c, i, j)]
+    ORC_PAR
     for (int j = 0; j < ny; ++j)
         for (int i = 1; i <= nx - 1; ++i) {
             double ue = 0.5 * (U(i, j) + U(i + 1, j));
@@ -290,6 +303,7 @@ static void convection(const orc_ctx *c, const double *u, const double *v, doubl
             }
             cu[UI(c, i, j)] = (ue * ue - uw * uw) / hxc[i] + (tn - ts) / dy[j];
         }
+    ORC_PAR
     for (int j = 1; j <= ny - 1; ++j)
         for (int i = 0; i < nx; ++i) {
             double vn = 0.5 * (V(i, j) + V(i, j + 1));
@@ -341,9 +355,21 @@ static int sor_run(int nsys, sor_sys *sys, double omega, double tol, int maxit,
     *status = ORC_OK;
     for (k = 1;; ++k) {
         rho = 0.0;
+        int rho_nan = 0;
         for (int colour = 0; colour < 2; ++colour)
             for (int s = 0; s < nsys; ++s) {
                 sor_sys *S = &sys[s];
+                /* rows of one colour are independent: the OpenMP build splits them over
+                 * threads; max and NaN are order-independent, so both builds agree bitwise */
+#ifdef _OPENMP
+#pragma omp parallel
+#endif
+                {
+                double trho = 0.0;
+                int tnan = 0;
+#ifdef _OPENMP
+#pragma omp for schedule(static)
+#endif
                 for (int j = 0; j < S->nj; ++j)
                     for (int i = 0; i < S->ni; ++i) {
                         if (((i + j) & 1) != colour) continue;
@@ -371,10 +397,19 @@ static int sor_run(int nsys, sor_sys *sys, double omega, double tol, int maxit,
                             S->x[id] = (1.0 - omega) * xo + omega * gs;
                         }
                         double e = fabs(d);
-                        if (isnan(e) || isnan(rho)) rho = NAN;
-                        else if (e > rho) rho = e;
+                        if (isnan(e)) tnan = 1;
+                        else if (e > trho) trho = e;
                     }
+#ifdef _OPENMP
+#pragma omp critical
+#endif
+                {
+                    if (tnan) rho_nan = 1;
+                    if (trho > rho) rho = trho;
+                }
+                }
             }
+        if (rho_nan) rho = NAN;
         if (isnan(rho)) { *status = ORC_ERR_DIVERGED; break; }
         if ((k % check_every == 0 && rho <= tol)) break;
         if (k == maxit) { *status = ORC_WARN_NOCONV; break; }
@@ -397,8 +432,10 @@ int orc_sor_generic(int ni, int nj, const double *aP, const double *aE, const do
 static void build_masks(orc_ctx *c)
 {
     int nx = c->nx, ny = c->ny;
+    ORC_PAR
     for (int j = 0; j < ny; ++j)
         for (int i = 0; i < nx; ++i) c->act[PI_(c, i, j)] = (c->tp[PI_(c, i, j)] == FLUID);
+    ORC_PAR
     for (int j = 0; j < ny; ++j)
         for (int i = 0; i <= nx; ++i) {
             int o = 0;
@@ -406,6 +443,7 @@ static void build_masks(orc_ctx *c)
                 o = c->tu[UI(c, i, j)] == FLUID && c->act[PI_(c, i - 1, j)] && c->act[PI_(c, i, j)];
             c->open_u[UI(c, i, j)] = (unsigned char)o;
         }
+    ORC_PAR
     for (int j = 0; j <= ny; ++j)
         for (int i = 0; i < nx; ++i) {
             int o = 0;
@@ -414,6 +452,7 @@ static void build_masks(orc_ctx *c)
             c->open_v[VI(c, i, j)] = (unsigned char)o;
         }
     /* R18: an active cell whose Poisson diagonal is 0 (no open face, no Dirichlet face) is inactive */
+    ORC_PAR
     for (int j = 0; j < ny; ++j)
         for (int i = 0; i < nx; ++i) {
             if (!c->act[PI_(c, i, j)]) continue;
@@ -435,6 +474,7 @@ static int poisson_solve(orc_ctx *c, const double *b, double *phi, double *rho, 
     int nx = c->nx, ny = c->ny;
     size_t n = (size_t)nx * ny;
     double *aP = dalloc(n), *aE = dalloc(n), *aW = dalloc(n), *aN = dalloc(n), *aS = dalloc(n);
+    ORC_PAR
     for (int j = 0; j < ny; ++j)
         for (int i = 0; i < nx; ++i) {
             size_t id = PI_(c, i, j);
@@ -620,6 +660,7 @@ static int step_once(orc_ctx *c)
     /* a2/a3: Helmholtz rhs (Fluid), targets (Forcing), body velocity (Solid), f (R19) */
     for (size_t id = 0; id < nu; ++id) { c->us[id] = c->u[id]; c->rhs_u[id] = 0.0; c->fu[id] = 0.0; }
     for (size_t id = 0; id < nv; ++id) { c->vs[id] = c->v[id]; c->rhs_v[id] = 0.0; c->fv[id] = 0.0; }
+    ORC_PAR
     for (int j = 0; j < ny; ++j)
         for (int i = 1; i <= nx - 1; ++i) {
             size_t id = UI(c, i, j);
@@ -638,6 +679,7 @@ static int step_once(orc_ctx *c)
                 c->fu[id] = (tgt - uhat) / dt;
             }
         }
+    ORC_PAR
     for (int j = 1; j <= ny - 1; ++j)
         for (int i = 0; i < nx; ++i) {
             size_t id = VI(c, i, j);
@@ -661,6 +703,7 @@ static int step_once(orc_ctx *c)
         double *aPu = dalloc(nu), *aEu = dalloc(nu), *aWu = dalloc(nu), *aNu = dalloc(nu), *aSu = dalloc(nu);
         double *aPv = dalloc(nv), *aEv = dalloc(nv), *aWv = dalloc(nv), *aNv = dalloc(nv), *aSv = dalloc(nv);
         unsigned char *updu = balloc(nu), *updv = balloc(nv);
+        ORC_PAR
         for (int j = 0; j < ny; ++j)
             for (int i = 0; i <= nx; ++i) {
                 size_t id = UI(c, i, j);
@@ -670,6 +713,7 @@ static int step_once(orc_ctx *c)
                 aPu[id] = 1.0 + beta * (((cE + cW) + (cN + cS)) + cD);
                 updu[id] = (i >= 1 && i <= nx - 1 && c->tu[id] == FLUID);
             }
+        ORC_PAR
         for (int j = 0; j <= ny; ++j)
             for (int i = 0; i < nx; ++i) {
                 size_t id = VI(c, i, j);
@@ -698,6 +742,7 @@ static int step_once(orc_ctx *c)
 
     tick(c, 2, &t0);
     /* a5: mass source q and Poisson rhs on the masks built above (R16) */
+    ORC_PAR
     for (int j = 0; j < ny; ++j)
         for (int i = 0; i < nx; ++i) {
             size_t id = PI_(c, i, j);
@@ -722,6 +767,7 @@ static int step_once(orc_ctx *c)
 
     tick(c, 4, &t0);
     /* a7: projection / correction (R9, R16, R17) */
+    ORC_PAR
     for (int j = 0; j < ny; ++j)
         for (int i = 0; i <= nx; ++i) {
             size_t id = UI(c, i, j);
@@ -735,6 +781,7 @@ static int step_once(orc_ctx *c)
             }
             c->u[id] = val;
         }
+    ORC_PAR
     for (int j = 0; j <= ny; ++j)
         for (int i = 0; i < nx; ++i) {
             size_t id = VI(c, i, j);
@@ -748,6 +795,7 @@ static int step_once(orc_ctx *c)
     /* R17b: an inactive cell with at least one active 4-neighbour takes the mean of
      * their p^{n+1} (E, W, N, S order, left fold); deeper inactive cells keep p.  Reads
      * active cells only, so the result does not depend on the loop order. */
+    ORC_PAR
     for (int j = 0; j < ny; ++j)
         for (int i = 0; i < nx; ++i) {
             if (c->act[PI_(c, i, j)]) continue;

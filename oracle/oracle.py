@@ -16,27 +16,39 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "ibm_oracle.c")
-LIB = os.path.join(HERE, "libibm_oracle.so")
+LIB = os.path.join(HERE, "libibm_oracle.so")          # oracle_seq: one thread (the checker)
+LIB_OMP = os.path.join(HERE, "libibm_oracle_omp.so")  # oracle_omp: same source, -fopenmp (host baseline)
 
-# plain C, one thread, no FMA contraction, no fast-math (DESIGN.md §3 R13)
+# plain C, no FMA contraction, no fast-math (DESIGN.md §3 R13)
 CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared"]
 
 
+def _build_one(path, extra):
+    if not os.path.exists(path) or os.path.getmtime(path) < os.path.getmtime(SRC):
+        tmp = path + ".tmp%d" % os.getpid()
+        subprocess.check_call(["gcc", *CFLAGS, *extra, "-o", tmp, SRC, "-lm"])
+        os.replace(tmp, path)
+    return path
+
+
 def build(force: bool = False) -> str:
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
-        tmp = LIB + ".tmp%d" % os.getpid()
-        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, SRC, "-lm"])
-        os.replace(tmp, LIB)
-    return LIB
+    """Builds both oracle libraries (seq and OpenMP); returns the seq one."""
+    if force:
+        for p in (LIB, LIB_OMP):
+            if os.path.exists(p):
+                os.remove(p)
+    _build_one(LIB_OMP, ["-fopenmp"])
+    return _build_one(LIB, [])
 
 
-_lib = None
+_libs = {}
 
 
-def lib():
-    global _lib
-    if _lib is None:
-        L = C.CDLL(build())
+def lib(omp: bool = False):
+    """ctypes handle of oracle_seq (default) or oracle_omp (threads: OMP_NUM_THREADS)."""
+    if omp not in _libs:
+        build()
+        L = C.CDLL(LIB_OMP if omp else LIB)
         dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
         bp = np.ctypeslib.ndpointer(dtype=np.uint8, flags="C_CONTIGUOUS")
         d, i, vp = C.c_double, C.c_int, C.c_void_p
@@ -75,8 +87,8 @@ def lib():
                                       C.POINTER(d), C.POINTER(i)]
         L.orc_sor_generic.restype = i
         L.orc_set_sor_form.argtypes = [i]
-        _lib = L
-    return _lib
+        _libs[omp] = L
+    return _libs[omp]
 
 
 FIELDS = {"u": 0, "v": 1, "p": 2, "phi": 3, "fu": 4, "fv": 5, "q": 6, "cu_prev": 7,
@@ -124,11 +136,12 @@ class Oracle:
     """One oracle solver instance (mirrors the C-ABI calls of include/ibm.h)."""
 
     def __init__(self, xn, yn, Re, dt, omega_p=1.5, tol_p=1e-6, maxit_p=10000,
-                 omega_uv=1.2, tol_uv=1e-8, maxit_uv=1000, check_every=1):
+                 omega_uv=1.2, tol_uv=1e-8, maxit_uv=1000, check_every=1, omp=False):
         self.xn = np.ascontiguousarray(xn, dtype=np.float64)
         self.yn = np.ascontiguousarray(yn, dtype=np.float64)
         self.nx, self.ny = len(self.xn) - 1, len(self.yn) - 1
-        self._c = lib().orc_create(self.nx, self.ny, self.xn, self.yn, Re, dt, omega_p, tol_p,
+        self._L = lib(omp)
+        self._c = self._L.orc_create(self.nx, self.ny, self.xn, self.yn, Re, dt, omega_p, tol_p,
                                    maxit_p, omega_uv, tol_uv, maxit_uv, check_every)
         if not self._c:
             raise ValueError("oracle: invalid configuration")
@@ -136,7 +149,7 @@ class Oracle:
     def __del__(self):
         c = getattr(self, "_c", None)
         if c:
-            lib().orc_destroy(c)
+            self._L.orc_destroy(c)
             self._c = None
 
     def shape(self, name):
@@ -147,12 +160,12 @@ class Oracle:
         return {"u": (ny, nx + 1), "v": (ny + 1, nx), "p": (ny, nx)}[f]
 
     def set_body(self, a, b, x0, y0, hbar, k):
-        st = lib().orc_set_body(self._c, a, b, x0, y0, hbar, k)
+        st = self._L.orc_set_body(self._c, a, b, x0, y0, hbar, k)
         if st:
             raise ValueError("oracle: invalid body")
 
     def clear_body(self):
-        lib().orc_clear_body(self._c)
+        self._L.orc_clear_body(self._c)
 
     def set_fields(self, u=None, v=None, p=None):
         keep = []
@@ -165,58 +178,58 @@ class Oracle:
             keep.append(a)
             return a.ctypes.data
 
-        lib().orc_set_fields(self._c, ptr(u, "u"), ptr(v, "v"), ptr(p, "p"))
+        self._L.orc_set_fields(self._c, ptr(u, "u"), ptr(v, "v"), ptr(p, "p"))
 
     def step(self, nsteps=1):
         """Returns (status, stats[nsteps, 8]) with columns
         t, it_uv, it_p, rho_uv, rho_p, cd, cl, status."""
         stats = np.zeros((max(nsteps, 1), 8))
-        st = lib().orc_step(self._c, nsteps, stats)
+        st = self._L.orc_step(self._c, nsteps, stats)
         return st, stats[:nsteps]
 
     def get(self, name):
         if name in TAGS:
             out = np.zeros(self.shape(name), dtype=np.uint8)
-            lib().orc_get_tags(self._c, TAGS[name], out)
+            self._L.orc_get_tags(self._c, TAGS[name], out)
             return out
         out = np.zeros(self.shape(name))
-        lib().orc_get(self._c, FIELDS[name], out)
+        self._L.orc_get(self._c, FIELDS[name], out)
         return out
 
     def timers(self):
         """Region wall times (s) since the last call: flagging, predictor+forcing, U-V SOR,
         Poisson rhs, P SOR, correction, forces (Table 1 layout)."""
         out = np.zeros(7)
-        lib().orc_timers(self._c, out)
+        self._L.orc_timers(self._c, out)
         return out
 
     def forces(self):
         out = np.zeros(3)
-        lib().orc_forces(self._c, out)
+        self._L.orc_forces(self._c, out)
         return tuple(out)
 
     def classify_at(self, t):
-        lib().orc_classify_at(self._c, t)
+        self._L.orc_classify_at(self._c, t)
 
     def convection(self, u, v):
         cu = np.zeros(self.shape("u"))
         cv = np.zeros(self.shape("v"))
-        lib().orc_convection(self._c, np.ascontiguousarray(u, dtype=np.float64),
+        self._L.orc_convection(self._c, np.ascontiguousarray(u, dtype=np.float64),
                              np.ascontiguousarray(v, dtype=np.float64), cu, cv)
         return cu, cv
 
     def laplacian(self, fam, x):
         name = {0: "u", 1: "v", 2: "p"}[fam]
         out = np.zeros(self.shape(name))
-        lib().orc_laplacian(self._c, fam, np.ascontiguousarray(x, dtype=np.float64), out)
+        self._L.orc_laplacian(self._c, fam, np.ascontiguousarray(x, dtype=np.float64), out)
         return out
 
     def poisson(self, rhs, phi0=None):
         phi = np.zeros(self.shape("p")) if phi0 is None else np.ascontiguousarray(phi0, dtype=np.float64).copy()
         rho, st = C.c_double(0.0), C.c_int(0)
-        it = lib().orc_poisson(self._c, np.ascontiguousarray(rhs, dtype=np.float64), phi,
+        it = self._L.orc_poisson(self._c, np.ascontiguousarray(rhs, dtype=np.float64), phi,
                                C.byref(rho), C.byref(st))
         return phi, it, rho.value, st.value
 
     def forcing_target(self, fam, x, i, j):
-        return lib().orc_forcing_target(self._c, fam, np.ascontiguousarray(x, dtype=np.float64), i, j)
+        return self._L.orc_forcing_target(self._c, fam, np.ascontiguousarray(x, dtype=np.float64), i, j)

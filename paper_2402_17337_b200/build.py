@@ -13,7 +13,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libibm_b200.so")
-SOURCES = ["kernels.cu", "sor.cu", "sor_wf.cu", "api.cu"]
+SOURCES = ["kernels.cu", "sor.cu", "sor_wf.cu", "sor_tb.cu", "api.cu"]
 HEADERS = ["ibm_internal.h", "sor_common.cuh", os.path.join("..", "..", "include", "ibm.h")]
 
 NVCC_FLAGS = [

@@ -157,7 +157,7 @@ size_t carve(Ctx &c, char *base) {
     s.bp = cv.take<double>(np); s.q = cv.take<double>(np);
     s.tu = cv.take<uint8_t>(nu); s.tv = cv.take<uint8_t>(nv); s.tp = cv.take<uint8_t>(np);
     s.pf = cv.take<uint8_t>(np);
-    s.red = cv.take<double>(4);
+    s.red = cv.take<double>(4 + 4 * 64);  // 4 force sums + the per-CTA parts of k_forces_part
   }
   return cv.off + 256;
 }
@@ -470,6 +470,34 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
     }
     a.total_tiles = a.f[0].tiles_x * a.f[0].tiles_y + (a.nfam == 2 ? a.f[1].tiles_x * a.f[1].tiles_y : 0);
     grids[r] = sor_grid(a);
+  }
+  if (!helm && !mult && c.tb_m >= 2 && cfg.sor_batch <= 0) {
+    // mid-size grid: the resident, temporally blocked persistent solve (sor_tb.cu)
+    TbArgs a = c.tb;
+    Slab &s = c.sl[0];
+    a.xb[0] = s.phi[0];
+    a.xb[1] = s.phi[1];
+    a.b = s.bp;
+    a.flag = s.pf;
+    a.box = s.bpb;
+    a.s0 = s0;
+    a.omega = omega;
+    a.tol = tol;
+    a.maxit = maxit;
+    a.check_every = cfg.check_every;
+    a.rho_bits = c.rho_bits;
+    a.ctl = c.ctl;
+    CK(launch_sor_tb(a, c.stream));
+    ++c.launches;
+    CK(cudaMemcpyAsync(&c.h_ctl[0], c.ctl, sizeof(SorCtl), cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    *k_out = c.h_ctl[0].k_done;
+    unsigned long long rb = c.h_ctl[0].rho_final;
+    std::memcpy(rho_out, &rb, sizeof(double));
+    *status = c.h_ctl[0].status;
+    *buf_out = c.h_ctl[0].buf;
+    if (iters_override <= 0) c.hint_p = *k_out;
+    return IBM_OK;
   }
   if (!mult && iters_override <= 0 && cfg.sor_batch <= 0 && sor_coop_fits(args[0])) {
     // small grid: the whole loop in one persistent cooperative launch
@@ -919,6 +947,24 @@ int ibm_init(const ibm_config *cfg, void *d_workspace, size_t bytes, void *cuda_
   for (auto &e : c.tev)
     if (cudaEventCreate(&e) != cudaSuccess) { c.err = "cudaEventCreate failed"; return fail(IBM_ERR_CUDA); }
   c.wf_L = 0;
+  // mid-size single-slab grids without the fused pass: resident temporally blocked
+  // Poisson solve when its tiles fit the co-resident grid (IBM_SOR_TB=0 disables,
+  // IBM_SOR_TB=m picks the iterations per grid barrier, default 4)
+  c.tb_m = 0;
+  {
+    const char *e = std::getenv("IBM_SOR_TB");
+    const int m = e ? std::atoi(e) : 4;
+    if (m >= 2 && c.wf_m == 1 && c.sl.size() == 1 && c.nranks == 1) {
+      int sms = 0;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
+      std::memset(&c.tb, 0, sizeof(c.tb));
+      const Slab &s = c.sl[0];
+      c.tb.g = s.gp;
+      c.tb.cE = c.m.cEp; c.tb.cW = c.m.cWp; c.tb.cD = c.m.cDp; c.tb.cN = c.m.cNp; c.tb.cS = c.m.cSp;
+      c.tb.ui0 = 0; c.tb.ui1 = c.nx; c.tb.uj0 = 0; c.tb.uj1 = c.ny;
+      if (sms > 0 && tb_plan(c.tb, c.nx, s.gp.nj, m, sms)) c.tb_m = m;
+    }
+  }
   HostMetric h = host_metric(*cfg);
   c.h_xn = nullptr;
   c.h_yn = nullptr;
@@ -1141,6 +1187,7 @@ int ibm_query(const ibm_ctx *ctx, int key, int *out) {
     case IBM_QUERY_WF_M: *out = ctx->wf_m; return IBM_OK;
     case IBM_QUERY_WF_L: *out = ctx->wf_L; return IBM_OK;
     case IBM_QUERY_SLABS: *out = (int)ctx->sl.size(); return IBM_OK;
+    case IBM_QUERY_TB_M: *out = ctx->tb_m; return IBM_OK;
   }
   return IBM_ERR_ARG;
 }

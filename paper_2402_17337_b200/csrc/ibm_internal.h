@@ -65,7 +65,7 @@ struct SorCtl {  // per-solve device control block
   int k_done;                    // -1 until converged / stopped
   int status;                    // 0 converged, 1 maxit, 3 NaN, 4 provisional (k_sor_wf lower bound; host confirms)
   unsigned ticket;               // last-block counter
-  int pad;
+  int buf;                       // k_sor_tb: ping-pong buffer holding the result
   unsigned long long rho3[3];    // persistent (cooperative) solve: residual of iteration k in slot k % 3
 };
 
@@ -104,6 +104,27 @@ struct WfArgs {
 };
 constexpr int kWfMaxM = 4;  // fused iterations per pass: 2..kWfMaxM instantiated
 
+// Persistent shared-memory-resident Poisson solve with m iterations per grid
+// barrier (sor_tb.cu; mid-size grids, one slab).  One CTA per tile of tx x ty
+// owned cells (ntx x nty tiles), for the whole solve.
+struct TbArgs {
+  double *xb[2];        // ping-pong iterate buffers
+  const double *b;
+  const uint8_t *flag;  // Poisson cell flags (valid inside box)
+  Geo g;
+  BBox box;
+  const double *cE, *cW, *cD, *cN, *cS;
+  int ui0, ui1, uj0, uj1;
+  int tx, ty, ntx, nty, m;
+  int s0;               // buffer holding the initial iterate
+  double omega, tol;
+  int maxit, check_every;
+  unsigned long long *rho_bits;
+  SorCtl *ctl;
+};
+bool tb_plan(TbArgs &a, int nx, int nj, int m, int sms);
+cudaError_t launch_sor_tb(const TbArgs &a, cudaStream_t st);
+
 struct Metric {  // device pointers, global index space
   double *xn, *yn, *dx, *dy, *xc, *yc, *hxc, *hyc;
   double *cEu, *cWu, *cDu, *cNu, *cSu;
@@ -123,7 +144,7 @@ struct Slab {
   double *u, *v, *p, *phi[2], *cu, *cv, *cup, *cvp, *us[2], *vs[2], *ru, *rv, *bp, *fu, *fv, *q;
   uint8_t *tu, *tv, *tp, *pf;
   BBox bu, bv, bpb;  // body envelope boxes (local rows incl. ghosts), empty without body
-  double *red;       // force partial sums [4]
+  double *red;       // force sums [4], then the 4 x 64 per-CTA parts of k_forces_part
   // TMA descriptors of the SOR operands (built once at init)
   CUtensorMap tm_phi[2], tm_bp, tm_us[2], tm_ru, tm_vs[2], tm_rv;
   CUtensorMap tm_wphi[2], tm_wbp;  // boxes of the temporally blocked Poisson pass (rows 2 wf_m + 2)
@@ -152,6 +173,8 @@ struct Ctx {
   int hint_uv, hint_p;
   int wf_m;         // Poisson iterations fused per HBM pass (1 = unfused k_sor)
   int wf_L;         // fused-pass segment length chosen by the online tuner (0: not yet)
+  int tb_m;         // iterations per grid barrier of the resident mid-grid solve (0: not used)
+  TbArgs tb;        // its tile plan (built at init)
   cudaEvent_t tev[12];  // tuner: start / stop of the first fused passes of a run
   int launches;     // kernels launched in the current step
   cudaEvent_t ev[8];

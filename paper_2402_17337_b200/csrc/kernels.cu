@@ -414,36 +414,40 @@ __global__ void k_pext(double *__restrict__ p, const double *__restrict__ phi, c
 
 // ---------------------------------------------------------------- a8: forces (R20, R19b)
 // red[0] = sum_{Solid,Forcing} f_u dV, red[1] = sum_{Solid,Forcing} u dV, red[2], red[3] for v.
-// One CTA over the body boxes: fixed reduction order (deterministic).
-__global__ void __launch_bounds__(512) k_forces(const double *__restrict__ u, const double *__restrict__ v,
-                                                const double *__restrict__ fu, const double *__restrict__ fv,
-                                                const uint8_t *__restrict__ tu, const uint8_t *__restrict__ tv,
-                                                Geo gu, Geo gv, BBox bu, BBox bv, Metric m, int nx, int ny,
-                                                double *red) {
-  __shared__ double sh[4][512];
+// Deterministic two-level reduction: CTA b of kForceParts sums a fixed contiguous
+// chunk of the body boxes' nodes (fixed tree order) into part[q][b]; one CTA then
+// sums the parts in order.
+constexpr int kForceParts = 64, kForceThreads = 256;
+__global__ void __launch_bounds__(kForceThreads) k_forces_part(const double *__restrict__ u,
+                                                               const double *__restrict__ v,
+                                                               const double *__restrict__ fu,
+                                                               const double *__restrict__ fv,
+                                                               const uint8_t *__restrict__ tu,
+                                                               const uint8_t *__restrict__ tv, Geo gu, Geo gv,
+                                                               BBox bu, BBox bv, Metric m, int nx, int ny,
+                                                               double *part) {
+  __shared__ double sh[4][kForceThreads];
+  const int wu = bu.i1 - bu.i0, nu = wu > 0 ? wu * (bu.j1 - bu.j0) : 0;
+  const int wv = bv.i1 - bv.i0, nv = wv > 0 ? wv * (bv.j1 - bv.j0) : 0;
+  const int n = nu + nv, chunk = (n + kForceParts - 1) / kForceParts;
+  const int lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  {
-    const int w = bu.i1 - bu.i0, n = w * (bu.j1 - bu.j0);
-    for (int idx = threadIdx.x; idx < n && w > 0; idx += blockDim.x) {
-      const int i = bu.i0 + idx % w, jl = bu.j0 + idx / w;
+  for (int idx = lo + threadIdx.x; idx < hi; idx += kForceThreads) {
+    if (idx < nu) {
+      const int i = bu.i0 + idx % wu, jl = bu.j0 + idx / wu;
       if (i < 1 || i > nx - 1 || jl < 0 || jl >= gu.nj) continue;
       const long o = gu.off(i, jl);
-      const uint8_t t = tu[o];
-      if (t == FLUID) continue;
+      if (tu[o] == FLUID) continue;
       const double dV = m.hxc[i] * m.dy[gu.gj0 + jl];
       s1 = s1 + u[o] * dV;
       s0 = s0 + fu[o] * dV;
-    }
-  }
-  {
-    const int w = bv.i1 - bv.i0, n = w * (bv.j1 - bv.j0);
-    for (int idx = threadIdx.x; idx < n && w > 0; idx += blockDim.x) {
-      const int i = bv.i0 + idx % w, jl = bv.j0 + idx / w;
+    } else {
+      const int k = idx - nu;
+      const int i = bv.i0 + k % wv, jl = bv.j0 + k / wv;
       const int gj = gv.gj0 + jl;
       if (gj < 1 || gj > ny - 1 || jl < 0 || jl >= gv.nj) continue;
       const long o = gv.off(i, jl);
-      const uint8_t t = tv[o];
-      if (t == FLUID) continue;
+      if (tv[o] == FLUID) continue;
       const double dV = m.dx[i] * m.hyc[gj];
       s3 = s3 + v[o] * dV;
       s2 = s2 + fv[o] * dV;
@@ -454,12 +458,20 @@ __global__ void __launch_bounds__(512) k_forces(const double *__restrict__ u, co
   sh[2][threadIdx.x] = s2;
   sh[3][threadIdx.x] = s3;
   __syncthreads();
-  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+  for (int st = kForceThreads / 2; st > 0; st >>= 1) {
     if (threadIdx.x < st)
       for (int q = 0; q < 4; ++q) sh[q][threadIdx.x] = sh[q][threadIdx.x] + sh[q][threadIdx.x + st];
     __syncthreads();
   }
-  if (threadIdx.x < 4) red[threadIdx.x] = sh[threadIdx.x][0];
+  if (threadIdx.x < 4) part[threadIdx.x * kForceParts + blockIdx.x] = sh[threadIdx.x][0];
+}
+
+__global__ void k_forces_final(const double *__restrict__ part, double *red) {
+  const int q = threadIdx.x;
+  if (q >= 4) return;
+  double s = 0.0;
+  for (int b = 0; b < kForceParts; ++b) s = s + part[q * kForceParts + b];
+  red[q] = s;
 }
 
 // fill the owned rows of a family with a constant (initial condition)
@@ -565,9 +577,10 @@ void launch_fill(double *p, const Geo &g, double val, cudaStream_t st) {
 }
 
 int launch_forces(const Ctx &c, const Slab &s) {
-  k_forces<<<1, 512, 0, c.stream>>>(s.u, s.v, s.fu, s.fv, s.tu, s.tv, s.gu, s.gv, s.bu, s.bv, c.m, c.nx, c.ny,
-                                     s.red);
-  return 1;
+  k_forces_part<<<kForceParts, kForceThreads, 0, c.stream>>>(s.u, s.v, s.fu, s.fv, s.tu, s.tv, s.gu, s.gv, s.bu, s.bv,
+                                                             c.m, c.nx, c.ny, s.red + 4);
+  k_forces_final<<<1, 32, 0, c.stream>>>(s.red + 4, s.red);
+  return 2;
 }
 
 }  // namespace ibm

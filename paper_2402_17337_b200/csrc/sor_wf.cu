@@ -54,22 +54,21 @@ constexpr unsigned FULL = 0xffffffffu;
 #endif
 constexpr int WNW = WF_NW;  // warps per CTA (independent work items)
 constexpr int WNT = 32 * WNW;
-// TMA prefetch distance (chunks in flight ahead of the one being computed) and
-// stages per warp.  A stage is refilled only after the chunk that follows its
-// own has been computed: the last row's b of a chunk is loaded from shared
-// memory in that chunk but first used at the start of the next one, so the
-// generic-proxy reads of the stage have all returned their values (been
-// consumed) before the async-proxy (TMA) write is issued -- no cross-proxy
-// write-after-read race, without a proxy fence.  Hence one stage more than the
-// prefetch distance.
+// TMA stages per warp (double buffering).  Chunk c + 1 is loaded into the stage
+// of chunk c - 1 once step 0 of chunk c has read that stage's last b row: from
+// then on no generic-proxy read of the stage is outstanding (every lane consumed
+// its values before the __syncwarp that precedes the issue), so the async-proxy
+// (TMA) write cannot race them -- without a proxy fence (a MEMBAR.ALL.CTA that
+// would also drain the warp's stores).  Lead: one chunk minus one row.
+template <int WM>
+__host__ __device__ constexpr int wf_nstg() {
+  return 2;
+}
+// prefetch distance of the four-columns-per-lane kernel below (half windows)
 #ifndef WF_PD
 #define WF_PD 2
 #endif
 constexpr int WPD = WF_PD;
-template <int WM>
-__host__ __device__ constexpr int wf_nstg() {
-  return WPD + 1;
-}
 #ifndef WF_NS
 #define WF_NS 1
 #endif
@@ -254,11 +253,16 @@ __device__ __forceinline__ void sfor(F &&f) {
 // (Compile-time ownership classes for the first / last two chunks of a segment
 // were measured 14 % slower overall: the extra rarely-run chunk bodies miss in
 // the instruction cache.)
-template <int WM, int TP, int MODE, bool OWN, bool APX>
+// Stage use: the chunk reads its own stage S and, at step 0, the b row rb-1 from
+// the previous chunk's stage Sp; `after0` runs once step 0 is done -- from then on
+// Sp is no longer read (every lane has consumed its values: __syncwarp inside), so
+// the caller refills it there.
+template <int WM, int TP, int MODE, bool OWN, bool APX, class After0>
 __device__ __forceinline__ void wf_chunk(double2 (&X)[NS][2 * WM + 2], double2 (&B)[NS][2 * WM + 2],
-                                         const WfStage<WM> &S, const WfCols &C, const WfArgs &A, int rb, int j0,
-                                         int j1, int i0, const bool (&lane_own)[NS], bool hasf, double cN0,
-                                         double cS0, unsigned long long (&tmax)[WM][NS]) {
+                                         const WfStage<WM> &S, const WfStage<WM> &Sp, const WfCols &C,
+                                         const WfArgs &A, int rb, int j0, int j1, int i0, const bool (&lane_own)[NS],
+                                         bool hasf, double cN0, double cS0, unsigned long long (&tmax)[WM][NS],
+                                         After0 &&after0) {
   constexpr int W = 2 * WM + 2;
   const int l = threadIdx.x & 31;
   const double omega = A.omega, omc = A.omc;
@@ -267,10 +271,14 @@ __device__ __forceinline__ void wf_chunk(double2 (&X)[NS][2 * WM + 2], double2 (
   double *const ob = A.xout + (long)(rb - 2 * WM + kGhost) * pitch + (i0 + 2 * l);
   sfor<W>([&](auto qc) {
     constexpr int q = decltype(qc)::value;
+    // row rb+q enters the window; the b of row rb+q-1 (first needed in this step)
+    // is read now rather than with its x one step earlier (one row less live)
+    constexpr int qb = (q + W - 1) % W;
 #pragma unroll
     for (int st = 0; st < NS; ++st) {
       X[st][q] = *reinterpret_cast<const double2 *>(&S.x[q][2 * (l + 32 * st)]);
-      B[st][q] = *reinterpret_cast<const double2 *>(&S.b[q][2 * (l + 32 * st)]);
+      B[st][qb] = *reinterpret_cast<const double2 *>(q == 0 ? &Sp.b[W - 1][2 * (l + 32 * st)]
+                                                             : &S.b[q == 0 ? 0 : q - 1][2 * (l + 32 * st)]);
     }
     sfor<2 * WM>([&](auto hc) {
       constexpr int h = decltype(hc)::value;
@@ -299,6 +307,7 @@ __device__ __forceinline__ void wf_chunk(double2 (&X)[NS][2 * WM + 2], double2 (
       st_pred(rowin && lane_own[st] && pair_in, ob + q * pitch + 64 * st, v);
       if (MODE < 2) st_pred1(rowin && lane_own[st] && !pair_in, ob + q * pitch + 64 * st, v.x);
     }
+    if constexpr (q == 0) after0();
   });
 }
 
@@ -346,18 +355,16 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
     if (l == 0) {
       for (int s = 0; s < NSTG; ++s) mbar_init(&bar[s], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      for (int c = 0; c < WPD && c < nch; ++c) {
-        mbar_expect_tx(&bar[c], kBytes);
-        tma_load_2d(&st[c].x[0][0], &A.tmx, i0, rs + c * W + kGhost, &bar[c]);
-        tma_load_2d(&st[c].b[0][0], &A.tmb, i0, rs + c * W + kGhost, &bar[c]);
-      }
+      mbar_expect_tx(&bar[0], kBytes);  // chunk 0; chunk c + 1 is issued inside chunk c
+      tma_load_2d(&st[0].x[0][0], &A.tmx, i0, rs + kGhost, &bar[0]);
+      tma_load_2d(&st[0].b[0][0], &A.tmb, i0, rs + kGhost, &bar[0]);
     }
     __syncwarp();
     // converged at an earlier iteration: nothing to do.  Tested after the first
     // TMA issue so that the control-word round trip does not delay the item's
     // first chunk; the loads in flight are waited for before leaving.
     if (*(volatile int *)&A.ctl->k_done >= 0) {
-      for (int c = 0; c < WPD && c < nch; ++c) mbar_wait_warp(&bar[c], 0);
+      mbar_wait_warp(&bar[0], 0);
       return;
     }
     bool lane_own[NS];
@@ -412,29 +419,34 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
     irr0 = __reduce_min_sync(FULL, irr0);
     irr1 = __reduce_max_sync(FULL, irr1);
     for (int c = 0; c < nch; ++c) {
-      const int s = c % NSTG;
+      const int s = c & 1;
       const int rb = rs + c * W;
       const bool fast = rb + W - 2 < irr0 || rb - 2 * WM > irr1;
       const bool hasf = boxstrip && rb + W - 2 >= A.box.j0 && rb - 2 * WM < A.box.j1;
-      mbar_wait_warp(&bar[s], (c / NSTG) & 1);
+      mbar_wait_warp(&bar[s], (c >> 1) & 1);
       const bool ownall = rb - 2 * WM >= j0 && rb + W - 2 < j1;
+      // after step 0: load chunk c + 1 into the other stage (see wf_nstg; for
+      // c = 0 that stage only supplied the b of the junk row rs - 1)
+      auto refill = [&]() {
+        __syncwarp();
+        if (l == 0 && c + 1 < nch) {
+          mbar_expect_tx(&bar[s ^ 1], kBytes);
+          tma_load_2d(&st[s ^ 1].x[0][0], &A.tmx, i0, rs + (c + 1) * W + kGhost, &bar[s ^ 1]);
+          tma_load_2d(&st[s ^ 1].b[0][0], &A.tmb, i0, rs + (c + 1) * W + kGhost, &bar[s ^ 1]);
+        }
+      };
       if (fast && interior && ownall)
-        wf_chunk<WM, TP, 2, true, APX>(X, B, st[s], C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax);
+        wf_chunk<WM, TP, 2, true, APX>(X, B, st[s], st[s ^ 1], C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax,
+                                       refill);
       else if (fast && interior)
-        wf_chunk<WM, TP, 2, false, APX>(X, B, st[s], C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax);
+        wf_chunk<WM, TP, 2, false, APX>(X, B, st[s], st[s ^ 1], C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax,
+                                        refill);
       else if (fast)
-        wf_chunk<WM, TP, 1, false, APX>(X, B, st[s], C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax);
+        wf_chunk<WM, TP, 1, false, APX>(X, B, st[s], st[s ^ 1], C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax,
+                                        refill);
       else
-        wf_chunk<WM, TP, 0, false, APX>(X, B, st[s], C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax);
-      __syncwarp();
-      if (l == 0 && c + WPD < nch) {
-        // refill the stage of chunk c - 1 (see wf_nstg): every lane consumed the
-        // values it read from it before the __syncwarp above
-        const int sr = (c + WPD) % NSTG;
-        mbar_expect_tx(&bar[sr], kBytes);
-        tma_load_2d(&st[sr].x[0][0], &A.tmx, i0, rs + (c + WPD) * W + kGhost, &bar[sr]);
-        tma_load_2d(&st[sr].b[0][0], &A.tmb, i0, rs + (c + WPD) * W + kGhost, &bar[sr]);
-      }
+        wf_chunk<WM, TP, 0, false, APX>(X, B, st[s], st[s ^ 1], C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax,
+                                        refill);
     }
   }
   // residual of each fused iteration: warp -> CTA -> atomicMax on its bit pattern

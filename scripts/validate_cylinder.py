@@ -62,15 +62,20 @@ def main():
     ap.add_argument("--dt", type=float, default=0.02)
     ap.add_argument("--omega-p", type=float, default=1.9)
     ap.add_argument("--tol-p", type=float, default=1e-8)
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_cylinder"))
+    ap.add_argument("--nx", type=int, default=512)
+    ap.add_argument("--ny", type=int, default=384)
+    ap.add_argument("--maxit-p", type=int, default=10000)
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02_cylinder"))
     args = ap.parse_args()
     import paper_2402_17337_b200 as P
 
-    cfg = I.cfg2(steps=args.steps, omega_p=args.omega_p, tol_p=args.tol_p)
+    cfg = I.cfg2(nx=args.nx, ny=args.ny, steps=args.steps, omega_p=args.omega_p, tol_p=args.tol_p,
+                 maxit_p=args.maxit_p)
     cfg.dt = args.dt
     g = P.Solver(cfg.xn, cfg.yn, **cfg.solver_kwargs())
     g.set_body(*cfg.body_args())
     g.set_fields(*I.initial_fields(cfg.nx, cfg.ny, args.perturb))
+    tb_m = g.query("tb_m")
     rows, t0 = [], time.time()
     chunk = 100
     status = 0
@@ -90,6 +95,7 @@ def main():
            "cd_last": float(cd[-1]), "cd_surface_pressure_last": float(cdp), "cl_surface_pressure_last": float(clp),
            "St": St, "n_crossings": len(ups), "mean_cd_last_half": float(np.mean(cd[n0:])),
            "cl_amplitude_last_half": float(0.5 * (cl[n0:].max() - cl[n0:].min())),
+           "poisson_path": "resident k_sor_tb, %d iterations per grid barrier" % tb_m if tb_m else "k_sor / k_sor_coop",
            "it_p_mean": float(S[:, 2].mean()), "it_p_max": float(S[:, 2].max()), "it_uv_mean": float(S[:, 1].mean()),
            "reference_trend": "St 0.16-0.17, mean Cd 1.3-1.4 (Re=100 cylinder, external literature)"}
     os.makedirs(os.path.dirname(args.out), exist_ok=True)

@@ -303,3 +303,31 @@ def test_sor_contract_vs_plain_ieee(oracle_mod):
         rel = np.linalg.norm(f0[k] - f1[k]) / np.linalg.norm(f0[k])
         assert rel < 1e-12, (k, rel)
     assert not np.array_equal(f0["p"], f1["p"])  # the two forms really differ in rounding
+
+
+# ------------------------------------------------------------------ oracle_omp
+@pytest.mark.parametrize("case", ["cfg1", "stretched-cylinder"])
+def test_oracle_omp_bitwise_equal_seq(oracle_mod, case):
+    """The OpenMP build of the oracle (rows of one colour / disjoint writes split
+    over threads, sums kept serial) is bitwise identical to the one-thread build:
+    fields, iteration counts, residuals and forces."""
+    if case == "cfg1":
+        cfg = I.cfg1(steps=6)
+    else:
+        xn = I.stretched_axis(-3.0, 6.0, -0.8, 1.2, 1.0 / 40, 1.06)
+        yn = I.stretched_axis(-2.5, 2.5, -0.6, 0.6, 1.0 / 40, 1.06)
+        cfg = I.Config("stretched-cyl", xn, yn, Re=100.0, dt=2e-3, body=I.Body(a=0.4, b=0.4, hbar=0.1, k=3.0),
+                       steps=4, maxit_p=400, perturb=0.01)
+    u0, v0, p0 = I.initial_fields(cfg.nx, cfg.ny, cfg.perturb)
+    res = []
+    for omp in (False, True):
+        o = oracle_mod.Oracle(cfg.xn, cfg.yn, omp=omp, **cfg.solver_kwargs())
+        o.set_body(*cfg.body_args())
+        o.set_fields(u0, v0, p0)
+        st, stats = o.step(cfg.steps)
+        res.append((st, stats, {k: o.get(k) for k in ("u", "v", "p", "phi", "fu", "fv", "q")}))
+    (s0, t0, f0), (s1, t1, f1) = res
+    assert s0 == s1
+    assert np.array_equal(t0, t1)
+    for k in f0:
+        assert np.array_equal(f0[k], f1[k]), k
