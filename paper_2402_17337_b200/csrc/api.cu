@@ -962,7 +962,10 @@ int ibm_init(const ibm_config *cfg, void *d_workspace, size_t bytes, void *cuda_
       c.tb.g = s.gp;
       c.tb.cE = c.m.cEp; c.tb.cW = c.m.cWp; c.tb.cD = c.m.cDp; c.tb.cN = c.m.cNp; c.tb.cS = c.m.cSp;
       c.tb.ui0 = 0; c.tb.ui1 = c.nx; c.tb.uj0 = 0; c.tb.uj1 = c.ny;
-      if (sms > 0 && tb_plan(c.tb, c.nx, s.gp.nj, m, sms)) c.tb_m = m;
+      // (deeper blocking needs wider halos: fall back to fewer iterations per barrier
+      // when the tiles of m do not fit the co-resident grid)
+      for (int mm = std::min(m, 4); mm >= 2 && c.tb_m == 0 && sms > 0; --mm)
+        if (tb_plan(c.tb, c.nx, s.gp.nj, mm, sms)) c.tb_m = mm;
     }
   }
   HostMetric h = host_metric(*cfg);

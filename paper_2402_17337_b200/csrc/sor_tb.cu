@@ -42,7 +42,7 @@ constexpr int TBW = TBT / 32;
 
 struct TbLayout {  // byte offsets of the shared-memory arrays of one tile region RX x RY
   int RX, RY;
-  size_t x, b, rc, fl, cE, cW, cD, cN, cS, red, total;
+  size_t x, b, rc, fl, rp, cE, cW, cD, cN, cS, red, total;
 };
 
 __host__ __device__ inline TbLayout tb_layout(int tx, int ty, int M) {
@@ -61,6 +61,7 @@ __host__ __device__ inline TbLayout tb_layout(int tx, int ty, int M) {
   L.cS = o; o += (size_t)L.RY * 8;
   L.red = o; o += (size_t)TBW * 4 * 8;
   L.fl = o; o += (n + 15) / 16 * 16;
+  L.rp = o; o += ((size_t)L.RY + 15) / 16 * 16;
   L.total = o;
   return L;
 }
@@ -73,6 +74,7 @@ struct TbCtx {
   double *x, *b, *rc, *cE, *cW, *cD, *cN, *cS;
   unsigned long long *red;
   uint8_t *fl;
+  uint8_t *rp;  // per row: 1 if every cell of the row is updated with open faces (no flags to apply)
   int RX, RY, gi0, jl0, gj0;  // region origin: global column gi0, local row jl0 (global row gj0 + jl0)
 };
 
@@ -91,50 +93,57 @@ __device__ __forceinline__ int tb_ix(int x, int y) { return y * TB_RX + ((x & 1)
 #define TB_R 2
 #endif
 
-// One half-sweep h (colour h & 1: red = (i + j) even) over the region shrunk by
-// h + 1 rings.  RES: fold |d| of owned cells into t.
+// One half-sweep h (colour h & 1: red = (i + j) even) over rows h+1 .. RY-2-h.
+// Rows of a warp are 8 apart, so the colour's column parity e (column 2 lane + e)
+// is the same in all of them.  In the de-interleaved layout the cell is at
+// y*64 + 32e + lane and its west / east neighbours at o - 1 + e / o + e with
+// o = y*64 + 32(1-e) + lane.  Cells past the region's outermost ring are
+// recomputed from stale halo values like every other halo cell (never stored or
+// counted), so only x = 0 / 63 (lane 0 with e = 0, lane 31 with e = 1) are
+// skipped.  Rows whose 64 cells are all updated with open faces (rp) take the
+// flag-free path.  RES: fold |d| of owned cells into t.
 template <bool RES>
 __device__ __forceinline__ void tb_half(const TbCtx &T, int h, int M, double omega, const double (&cE2)[2],
                                         const double (&cW2)[2], unsigned long long &t) {
   constexpr int R = TB_R;  // rows per pass of a warp: their loads are issued before any store (ILP)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int y0 = h + 1, y1 = T.RY - 2 - h, x0 = h + 1, x1 = TB_RX - 2 - h;
+  const int y0 = h + 1, y1 = T.RY - 2 - h;
   const int H = 2 * M;
-  // the lane's column of this colour alternates with the row: (gi + gj + colour) even
-  const int ebase = (T.gi0 + T.gj0 + T.jl0 + (h & 1)) & 1;
+  const int e = (T.gi0 + T.gj0 + T.jl0 + (h & 1) + y0 + w) & 1;
+  const bool act = e ? lane != 31 : lane != 0;
+  const bool lres = RES && lane >= H / 2 && lane < 32 - H / 2;  // owned columns (x in [H, 64-H))
+  const double cE = e ? cE2[1] : cE2[0], cW = e ? cW2[1] : cW2[0];
+  const int offC = (e << 5) + lane, offO = ((e ^ 1) << 5) + lane + e;  // cell; east neighbour (west = -1)
   for (int yb = y0 + w; yb <= y1; yb += TBW * R) {
     double xo[R], nm[R];
     bool upd[R];
-    int id[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const int y = yb + r * TBW;
-      const int e = (ebase + y) & 1;
-      const int x = 2 * lane + e;
-      const bool in = y <= y1 && x >= x0 && x <= x1;
-      const int yy = in ? y : 1, xx = in ? x : 1;  // (a valid dummy cell when out of range)
-      const int i = tb_ix(xx, yy);
-      const uint8_t f = T.fl[i];
-      upd[r] = in && (f & TB_UPD);
-      id[r] = i;
-      const double aE = (f & PF_E) ? 0.0 : (e ? cE2[1] : cE2[0]);  // (selects: no local-memory array)
-      const double aW = (f & PF_W) ? 0.0 : (e ? cW2[1] : cW2[0]);
-      const double aN = (f & PF_N) ? 0.0 : T.cN[yy];
-      const double aS = (f & PF_S) ? 0.0 : T.cS[yy];
-      xo[r] = T.x[i];
-      nm[r] = __fma_rn(aN, T.x[i + TB_RX],
-                       __fma_rn(aE, T.x[tb_ix(xx + 1, yy)],
-                                __fma_rn(aW, T.x[tb_ix(xx - 1, yy)], __fma_rn(aS, T.x[i - TB_RX], T.b[i]))));
+      const int y = min(yb + r * TBW, y1);  // (a duplicate of the last row when past it: not stored)
+      const int iC = y * TB_RX + offC, iE = y * TB_RX + offO;
+      double aE = cE, aW = cW, aN = T.cN[y], aS = T.cS[y];
+      bool u = act && yb + r * TBW <= y1;
+      if (!T.rp[y]) {
+        const uint8_t f = T.fl[iC];
+        u = u && (f & TB_UPD);
+        aE = (f & PF_E) ? 0.0 : aE;
+        aW = (f & PF_W) ? 0.0 : aW;
+        aN = (f & PF_N) ? 0.0 : aN;
+        aS = (f & PF_S) ? 0.0 : aS;
+      }
+      upd[r] = u;
+      xo[r] = T.x[iC];
+      nm[r] = __fma_rn(aN, T.x[iC + TB_RX],
+                       __fma_rn(aE, T.x[iE], __fma_rn(aW, T.x[iE - 1], __fma_rn(aS, T.x[iC - TB_RX], T.b[iC]))));
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const double d = __fma_rn(nm[r], T.rc[id[r]], -xo[r]);
+      const int y = min(yb + r * TBW, y1);
+      const int iC = y * TB_RX + offC;
+      const double d = __fma_rn(nm[r], T.rc[iC], -xo[r]);
       if (upd[r]) {
-        T.x[id[r]] = __fma_rn(omega, d, xo[r]);
-        if (RES) {
-          const int y = yb + r * TBW, x = 2 * lane + ((ebase + y) & 1);
-          if (y >= H && y < T.RY - H && x >= H && x < TB_RX - H) t = umax64(t, abs_bits(d));
-        }
+        T.x[iC] = __fma_rn(omega, d, xo[r]);
+        if (RES && lres && y >= H && y < T.RY - H) t = umax64(t, abs_bits(d));
       }
     }
   }
@@ -193,6 +202,7 @@ __global__ void __launch_bounds__(TBT, 2) k_sor_tb(const __grid_constant__ TbArg
   T.cS = reinterpret_cast<double *>(smraw + L.cS);
   T.red = reinterpret_cast<unsigned long long *>(smraw + L.red);
   T.fl = smraw + L.fl;
+  T.rp = smraw + L.rp;
   T.RX = L.RX;  // == TB_RX (tb_plan)
   T.RY = L.RY;
   const Geo &g = A.g;
@@ -249,12 +259,18 @@ __global__ void __launch_bounds__(TBT, 2) k_sor_tb(const __grid_constant__ TbArg
   // column coefficients of the lane's two columns (registers for the whole solve)
   double cE2[2], cW2[2];
   {
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     __syncthreads();
     for (int e = 0; e < 2; ++e) {
       cE2[e] = T.cE[2 * lane + e];
       cW2[e] = T.cW[2 * lane + e];
     }
+    for (int y = w; y < T.RY; y += TBW) {  // rows without flags to apply
+      const bool plain = T.fl[tb_ix(2 * lane, y)] == TB_UPD && T.fl[tb_ix(2 * lane + 1, y)] == TB_UPD;
+      const bool all = __all_sync(0xffffffffu, plain);
+      if (lane == 0) T.rp[y] = all ? 1 : 0;
+    }
+    __syncthreads();
   }
   // ---- blocks of M iterations, one grid barrier each
   for (int k = 1;; k += M) {
