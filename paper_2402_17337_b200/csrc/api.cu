@@ -326,8 +326,9 @@ bool make_maps(Slab &s, int wf_m) {
 // ---------------------------------------------------------------- halos and reductions
 // exchange 2 ghost rows of one family buffer (selected per slab by `pick`)
 template <class Pick>
-int halo(Ctx &c, Pick pick, int rows = 2) {
+int halo(Ctx &c, Pick pick, int rows = 2, cudaStream_t st = nullptr, bool on_comm = false) {
   const size_t esz = sizeof(double);
+  if (!on_comm) st = c.stream;
   if (c.loopback) {
     for (size_t r = 0; r + 1 < c.sl.size(); ++r) {
       double *lo, *up;
@@ -336,14 +337,15 @@ int halo(Ctx &c, Pick pick, int rows = 2) {
       pick(c.sl[r + 1], &up, &gup);
       const size_t bytes = (size_t)rows * glo->pitch * esz;
       CK(cudaMemcpyAsync(up + gup->off(0, -rows), lo + glo->off(0, glo->nj - rows), bytes,
-                         cudaMemcpyDeviceToDevice, c.stream));
-      CK(cudaMemcpyAsync(lo + glo->off(0, glo->nj), up + gup->off(0, 0), bytes, cudaMemcpyDeviceToDevice,
-                         c.stream));
+                         cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(lo + glo->off(0, glo->nj), up + gup->off(0, 0), bytes, cudaMemcpyDeviceToDevice, st));
     }
     return IBM_OK;
   }
   if (c.nranks == 1) return IBM_OK;
-  ncclComm_t comm = (ncclComm_t)c.nccl;
+  // (the overlapped exchanges use their own communicator: NCCL operations of one
+  // communicator must not run concurrently on two streams)
+  ncclComm_t comm = (ncclComm_t)(on_comm ? c.nccl_halo : c.nccl);
   double *buf;
   const Geo *g;
   pick(c.sl[0], &buf, &g);
@@ -351,12 +353,12 @@ int halo(Ctx &c, Pick pick, int rows = 2) {
   const size_t cnt = (size_t)rows * g->pitch;
   NK(ncclGroupStart());
   if (r > 0) {
-    NK(ncclSend(buf + g->off(0, 0), cnt, ncclFloat64, r - 1, comm, c.stream));
-    NK(ncclRecv(buf + g->off(0, -rows), cnt, ncclFloat64, r - 1, comm, c.stream));
+    NK(ncclSend(buf + g->off(0, 0), cnt, ncclFloat64, r - 1, comm, st));
+    NK(ncclRecv(buf + g->off(0, -rows), cnt, ncclFloat64, r - 1, comm, st));
   }
   if (r < c.nranks - 1) {
-    NK(ncclSend(buf + g->off(0, g->nj - rows), cnt, ncclFloat64, r + 1, comm, c.stream));
-    NK(ncclRecv(buf + g->off(0, g->nj), cnt, ncclFloat64, r + 1, comm, c.stream));
+    NK(ncclSend(buf + g->off(0, g->nj - rows), cnt, ncclFloat64, r + 1, comm, st));
+    NK(ncclRecv(buf + g->off(0, g->nj), cnt, ncclFloat64, r + 1, comm, st));
   }
   NK(ncclGroupEnd());
   return IBM_OK;
@@ -372,6 +374,12 @@ int halo(Ctx &c, Pick pick, int rows = 2) {
   do {                                                                          \
     int st_ = halo(c, [&](Slab &s, double **b, const Geo **g) { expr; }, rows); \
     if (st_) return st_;                                                        \
+  } while (0)
+// ... on the comm stream with the halo communicator (overlapped with the pass)
+#define HALO_ROWS_COMM(rows, expr)                                                              \
+  do {                                                                                          \
+    int st_ = halo(c, [&](Slab &s, double **b, const Geo **g) { expr; }, rows, c.comm, true);   \
+    if (st_) return st_;                                                                        \
   } while (0)
 
 bool multi(const Ctx &c) { return c.sl.size() > 1 || c.nranks > 1; }
@@ -542,10 +550,19 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
     wa.multi = mult ? 1 : 0;
     wf_plan(wa, c.wf_m);
   }
+  // decomposed fused passes: an exchange of the last pass's output may be in
+  // flight on the comm stream; the main stream joins it before touching ghost rows
+  bool halo_ready = false;
+  auto join_comm = [&]() -> int {
+    if (halo_ready) CK(cudaStreamWaitEvent(c.stream, c.ev_halo, 0));
+    halo_ready = false;
+    return IBM_OK;
+  };
   // one single-iteration pass of every slab (halos first when decomposed)
   auto single = [&](int kk, int in, bool fixup) -> int {
     const int out = in ^ 1;
     if (mult) {
+      if (int e = join_comm()) return e;
       if (helm) {
         HALO((*b = s.us[in], *g = &s.gu));
         HALO((*b = s.vs[in], *g = &s.gv));
@@ -602,9 +619,44 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
   for (;;) {
     const int kend = std::min(maxit, k + batch - 1);
     while (k <= kend) {
-      if (wf && k + c.wf_m - 1 <= maxit) {
+      if (wf && mult && k + c.wf_m - 1 <= maxit) {
+        // Decomposed grid: the 2m halo rows of this pass's input arrived on the comm
+        // stream (the first pass: exchanged here); the edge segments (those that read
+        // ghost rows) run first, then the interior ones while the comm stream already
+        // exchanges the edge rows of this pass's output for the next pass.
         const int in = cur;
-        if (mult) HALO_ROWS(2 * c.wf_m, (*b = s.phi[in], *g = &s.gp));
+        if (!halo_ready) HALO_ROWS(2 * c.wf_m, (*b = s.phi[in], *g = &s.gp));
+        else CK(cudaStreamWaitEvent(c.stream, c.ev_halo, 0));
+        for (int mode = 1; mode <= 2; ++mode) {
+          for (size_t r = 0; r < c.sl.size(); ++r) {
+            WfArgs wa = was[r];
+            const int nseg = mode == 1 ? wa.e_lo + wa.e_hi : wa.segs - wa.e_lo - wa.e_hi;
+            if (nseg <= 0) continue;
+            wa.seg_mode = mode;
+            wa.items = wa.strips * nseg;
+            wa.k = k;
+            wa.xout = c.sl[r].phi[in ^ 1];
+            wa.tmx = c.sl[r].tm_wphi[in];
+            CK(launch_sor_wf(wa, c.wf_m, c.stream));
+            ++c.launches;
+          }
+          if (mode == 1) {
+            CK(cudaEventRecord(c.ev_edge, c.stream));
+            CK(cudaStreamWaitEvent(c.comm, c.ev_edge, 0));
+            HALO_ROWS_COMM(2 * c.wf_m, (*b = s.phi[in ^ 1], *g = &s.gp));
+            CK(cudaEventRecord(c.ev_halo, c.comm));
+            halo_ready = true;
+          }
+        }
+        if (!c.loopback)
+          NK(ncclAllReduce(c.rho_bits + k, c.rho_bits + k, c.wf_m, ncclUint64, ncclMax, (ncclComm_t)c.nccl,
+                           c.stream));
+        launch_sor_check(c.ctl, c.rho_bits, k, maxit, cfg.check_every, tol, c.stream, c.wf_m, wf_approx() ? 1 : 0);
+        ++c.launches;
+        passes.push_back({k, c.wf_m, cur});
+        k += c.wf_m;
+      } else if (wf && k + c.wf_m - 1 <= maxit) {
+        const int in = cur;
         const bool tuning = tune_launched < tune_n;
         if (tuning) {
           wf_plan(was[0], c.wf_m, cand[tune_launched % cand.size()]);
@@ -622,10 +674,7 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
           CK(cudaEventRecord(c.tev[2 * tune_launched + 1], c.stream));
           if (++tune_launched == tune_n) tune_k_end = k + c.wf_m - 1;
         }
-        if (mult && !c.loopback)
-          NK(ncclAllReduce(c.rho_bits + k, c.rho_bits + k, c.wf_m, ncclUint64, ncclMax, (ncclComm_t)c.nccl,
-                           c.stream));
-        // the decision of every fused pass (single slab too): first of its m iterations that may stop
+        // the decision of every fused pass: first of its m iterations that may stop
         launch_sor_check(c.ctl, c.rho_bits, k, maxit, cfg.check_every, tol, c.stream, c.wf_m, wf_approx() ? 1 : 0);
         ++c.launches;
         passes.push_back({k, c.wf_m, cur});
@@ -706,6 +755,7 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
       break;
     }
   if (buf < 0) { c.err = "SOR stopped at an iteration no pass covers"; return IBM_ERR_STATE; }
+  if (int e = join_comm()) return e;
   *buf_out = buf;
   if (iters_override <= 0) hint = *k_out;
   return IBM_OK;
@@ -912,12 +962,20 @@ int ibm_init(const ibm_config *cfg, void *d_workspace, size_t bytes, void *cuda_
   c.h_ctl = nullptr;
   c.h_red = nullptr;
   c.h_nan = nullptr;
+  c.comm = nullptr;
+  c.ev_edge = c.ev_halo = nullptr;
+  c.nccl_halo = nullptr;
   auto fail = [&](int code) {
     fprintf(stderr, "ibm_init: %s\n", c.err.c_str());
     for (auto &e : c.ev)
       if (e) cudaEventDestroy(e);
     for (auto &e : c.tev)
       if (e) cudaEventDestroy(e);
+    if (c.ev_edge) cudaEventDestroy(c.ev_edge);
+    if (c.ev_halo) cudaEventDestroy(c.ev_halo);
+    if (c.comm) cudaStreamDestroy(c.comm);
+    if (c.nccl_halo) ncclCommDestroy((ncclComm_t)c.nccl_halo);
+    if (c.nccl) ncclCommDestroy((ncclComm_t)c.nccl);
     if (c.h_ctl) cudaFreeHost(c.h_ctl);
     if (c.h_red) cudaFreeHost(c.h_red);
     if (c.h_nan) cudaFreeHost(c.h_nan);
@@ -946,6 +1004,14 @@ int ibm_init(const ibm_config *cfg, void *d_workspace, size_t bytes, void *cuda_
     if (cudaEventCreate(&e) != cudaSuccess) { c.err = "cudaEventCreate failed"; return fail(IBM_ERR_CUDA); }
   for (auto &e : c.tev)
     if (cudaEventCreate(&e) != cudaSuccess) { c.err = "cudaEventCreate failed"; return fail(IBM_ERR_CUDA); }
+  if (c.sl.size() > 1 || c.nranks > 1) {  // decomposed: the overlapped halo exchange of the fused pass
+    if (cudaStreamCreateWithFlags(&c.comm, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c.ev_edge, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c.ev_halo, cudaEventDisableTiming) != cudaSuccess) {
+      c.err = "comm stream / events";
+      return fail(IBM_ERR_CUDA);
+    }
+  }
   c.wf_L = 0;
   // mid-size single-slab grids without the fused pass: resident temporally blocked
   // Poisson solve when its tiles fit the co-resident grid (IBM_SOR_TB=0 disables,
@@ -1001,6 +1067,13 @@ int ibm_init(const ibm_config *cfg, void *d_workspace, size_t bytes, void *cuda_
       return fail(IBM_ERR_NCCL);
     }
     c.nccl = comm;
+    ncclComm_t halo_comm;
+    nr = ncclCommSplit(comm, 0, cfg->rank, &halo_comm, nullptr);
+    if (nr != ncclSuccess) {
+      c.err = std::string("ncclCommSplit: ") + ncclGetErrorString(nr);
+      return fail(IBM_ERR_NCCL);
+    }
+    c.nccl_halo = halo_comm;
   }
   c.body = Body{0, 0, 0, 0, 0, 0, 0};
   c.phi_cur = 0;
@@ -1205,7 +1278,12 @@ int ibm_destroy(ibm_ctx *ctx) {
   Ctx &c = *ctx;
   cudaSetDevice(c.device);
   cudaStreamSynchronize(c.stream);
+  if (c.comm) cudaStreamSynchronize(c.comm);
+  if (c.nccl_halo) ncclCommDestroy((ncclComm_t)c.nccl_halo);
   if (c.nccl) ncclCommDestroy((ncclComm_t)c.nccl);
+  if (c.ev_edge) cudaEventDestroy(c.ev_edge);
+  if (c.ev_halo) cudaEventDestroy(c.ev_halo);
+  if (c.comm) cudaStreamDestroy(c.comm);
   for (auto &e : c.ev) cudaEventDestroy(e);
   for (auto &e : c.tev) cudaEventDestroy(e);
   cudaFreeHost(c.h_ctl);

@@ -96,6 +96,10 @@ struct WfArgs {
   int ui0, ui1, uj0, uj1;
   int strips, segs, L, items;
   int order, order_mul, order_g;  // item -> (strip, segment) order: 2 strip-major (default), 0 row-major, 1 scattered
+  // segment subset of this launch (decomposed grids overlap the halo exchange with
+  // the interior): 0 all segments; 1 the edge segments -- the e_lo first and e_hi
+  // last ones, whose streamed rows reach the ghost rows; 2 the interior ones
+  int seg_mode, e_lo, e_hi;
   int multi;            // several slabs / ranks: the decision runs after the residual reduction
   double omega, omc, tol;
   int k, maxit, check_every;
@@ -179,6 +183,9 @@ struct Ctx {
   int launches;     // kernels launched in the current step
   cudaEvent_t ev[8];
   void *nccl;      // ncclComm_t when nranks > 1 and !loopback
+  void *nccl_halo; // its split for the halo exchanges on the comm stream (overlapped with the pass)
+  cudaStream_t comm;      // halo-exchange stream of the decomposed fused pass (nranks > 1 or loopback)
+  cudaEvent_t ev_edge, ev_halo;  // edge items of a pass done / its output's halo rows exchanged
   std::string err;
 };
 

@@ -54,15 +54,23 @@ constexpr unsigned FULL = 0xffffffffu;
 #endif
 constexpr int WNW = WF_NW;  // warps per CTA (independent work items)
 constexpr int WNT = 32 * WNW;
-// TMA stages per warp (double buffering).  Chunk c + 1 is loaded into the stage
-// of chunk c - 1 once step 0 of chunk c has read that stage's last b row: from
-// then on no generic-proxy read of the stage is outstanding (every lane consumed
-// its values before the __syncwarp that precedes the issue), so the async-proxy
-// (TMA) write cannot race them -- without a proxy fence (a MEMBAR.ALL.CTA that
-// would also drain the warp's stores).  Lead: one chunk minus one row.
+// TMA stages per warp.  A window of W = 2WM+2 rows arrives as two halves of WM+1
+// rows, each in its own stage (4 KB at WM = 3); four stages per warp (the 16 KB of
+// the old two full-window stages).  Half hc is read by its own steps and -- the b
+// of its last row -- by the first step of half hc+1; right after that step (behind
+// a __syncwarp: every lane has consumed the values it read) its stage is refilled
+// with half hc+4.  So no generic-proxy read of a stage is outstanding when the TMA
+// (async proxy) overwrites it -- no cross-proxy write-after-read race and no proxy
+// fence (MEMBAR.ALL.CTA + FENCE.VIEW.ASYNC.S, which would also drain the warp's
+// stores) -- and three halves (3 x 4 - 1 = 11 rows) are in flight ahead of the one
+// being computed (ncu: with one full window of lead, 33 % of the stall samples
+// waited for TMA data).
+#ifndef WF_NSTG
+#define WF_NSTG 4
+#endif
 template <int WM>
 __host__ __device__ constexpr int wf_nstg() {
-  return 2;
+  return WF_NSTG;
 }
 // prefetch distance of the four-columns-per-lane kernel below (half windows)
 #ifndef WF_PD
@@ -79,9 +87,9 @@ constexpr int SC = 64 * NS;  // stored columns per strip
 #endif
 
 template <int WM>
-struct __align__(128) WfStage {
-  double x[2 * WM + 2][SC];
-  double b[2 * WM + 2][SC];
+struct __align__(128) WfStage {  // half a window: rows rb + h (WM+1) .. + WM
+  double x[WM + 1][SC];
+  double b[WM + 1][SC];
 };
 template <int WM>
 constexpr size_t wf_smem() {
@@ -253,32 +261,35 @@ __device__ __forceinline__ void sfor(F &&f) {
 // (Compile-time ownership classes for the first / last two chunks of a segment
 // were measured 14 % slower overall: the extra rarely-run chunk bodies miss in
 // the instruction cache.)
-// Stage use: the chunk reads its own stage S and, at step 0, the b row rb-1 from
-// the previous chunk's stage Sp; `after0` runs once step 0 is done -- from then on
-// Sp is no longer read (every lane has consumed its values: __syncwarp inside), so
-// the caller refills it there.
-template <int WM, int TP, int MODE, bool OWN, bool APX, class After0>
+// Stage use: the chunk reads its two half-window stages SA, SB and, at step 0, the b row rb-1 from
+// the previous half's stage Sp; the hooks wait for the second half's stage and
+// refill a stage once it is no longer read (see wf_nstg).
+template <int WM, int TP, int MODE, bool OWN, bool APX, class Hooks>
 __device__ __forceinline__ void wf_chunk(double2 (&X)[NS][2 * WM + 2], double2 (&B)[NS][2 * WM + 2],
-                                         const WfStage<WM> &S, const WfStage<WM> &Sp, const WfCols &C,
-                                         const WfArgs &A, int rb, int j0, int j1, int i0, const bool (&lane_own)[NS],
-                                         bool hasf, double cN0, double cS0, unsigned long long (&tmax)[WM][NS],
-                                         After0 &&after0) {
+                                         const WfStage<WM> &SA, const WfStage<WM> &SB, const WfStage<WM> &Sp,
+                                         const WfCols &C, const WfArgs &A, int rb, int j0, int j1, int i0,
+                                         const bool (&lane_own)[NS], bool hasf, double cN0, double cS0,
+                                         unsigned long long (&tmax)[WM][NS], Hooks &&hooks) {
   constexpr int W = 2 * WM + 2;
   const int l = threadIdx.x & 31;
   const double omega = A.omega, omc = A.omc;
   const long pitch = A.g.pitch;
   // stored row rb + q - 2WM of this lane's first pair (the second is 64 columns on)
   double *const ob = A.xout + (long)(rb - 2 * WM + kGhost) * pitch + (i0 + 2 * l);
+  constexpr int CR = WM + 1;  // rows per half window (stage)
   sfor<W>([&](auto qc) {
     constexpr int q = decltype(qc)::value;
+    if constexpr (q == CR) hooks.wait_second();  // second half's stage has landed
     // row rb+q enters the window; the b of row rb+q-1 (first needed in this step)
     // is read now rather than with its x one step earlier (one row less live)
     constexpr int qb = (q + W - 1) % W;
+    const WfStage<WM> &Sx = q < CR ? SA : SB;
+    const WfStage<WM> &Sb = q == 0 ? Sp : (q - 1 < CR ? SA : SB);
+    constexpr int rx = q % CR, rbb = (q + W - 1) % W % CR;
 #pragma unroll
     for (int st = 0; st < NS; ++st) {
-      X[st][q] = *reinterpret_cast<const double2 *>(&S.x[q][2 * (l + 32 * st)]);
-      B[st][qb] = *reinterpret_cast<const double2 *>(q == 0 ? &Sp.b[W - 1][2 * (l + 32 * st)]
-                                                             : &S.b[q == 0 ? 0 : q - 1][2 * (l + 32 * st)]);
+      X[st][q] = *reinterpret_cast<const double2 *>(&Sx.x[rx][2 * (l + 32 * st)]);
+      B[st][qb] = *reinterpret_cast<const double2 *>(&Sb.b[rbb][2 * (l + 32 * st)]);
     }
     sfor<2 * WM>([&](auto hc) {
       constexpr int h = decltype(hc)::value;
@@ -307,14 +318,15 @@ __device__ __forceinline__ void wf_chunk(double2 (&X)[NS][2 * WM + 2], double2 (
       st_pred(rowin && lane_own[st] && pair_in, ob + q * pitch + 64 * st, v);
       if (MODE < 2) st_pred1(rowin && lane_own[st] && !pair_in, ob + q * pitch + 64 * st, v.x);
     }
-    if constexpr (q == 0) after0();
+    if constexpr (q == 0) hooks.after_first();  // the previous half's stage is no longer read
+    if constexpr (q == CR) hooks.after_second();  // this window's first half: no longer read
   });
 }
 
 template <int WM, int TP, bool APX>
 __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __grid_constant__ WfArgs A) {
-  constexpr int W = 2 * WM + 2, OW = SC - 4 * WM, NSTG = wf_nstg<WM>();
-  constexpr unsigned kBytes = 2u * W * SC * 8;
+  constexpr int W = 2 * WM + 2, OW = SC - 4 * WM, NSTG = wf_nstg<WM>(), CR = WM + 1;
+  constexpr unsigned kBytes = 2u * CR * SC * 8;  // one half window of x and b
   extern __shared__ __align__(1024) unsigned char smraw[];
   __shared__ unsigned long long wmax[WNW][WM];
   const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -335,7 +347,15 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
     // height; measured 5-6 % faster than segment-row-major at 8192^2 (DRAM
     // pattern).  IBM_WF_ORDER=0: segment-row-major; 1: scattered rows.
     int sx = item / A.segs, sy = item % A.segs;
-    if (A.order == 0) {
+    if (A.seg_mode == 1) {  // edge segments only (strip-major)
+      const int ne = A.e_lo + A.e_hi, k = item % ne;
+      sx = item / ne;
+      sy = k < A.e_lo ? k : A.segs - A.e_hi + (k - A.e_lo);
+    } else if (A.seg_mode == 2) {  // interior segments only
+      const int ni_ = A.segs - A.e_lo - A.e_hi;
+      sx = item / ni_;
+      sy = A.e_lo + item % ni_;
+    } else if (A.order == 0) {
       sx = item % A.strips;
       sy = item / A.strips;
     } else if (A.order == 1) {
@@ -355,16 +375,18 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
     if (l == 0) {
       for (int s = 0; s < NSTG; ++s) mbar_init(&bar[s], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      mbar_expect_tx(&bar[0], kBytes);  // chunk 0; chunk c + 1 is issued inside chunk c
-      tma_load_2d(&st[0].x[0][0], &A.tmx, i0, rs + kGhost, &bar[0]);
-      tma_load_2d(&st[0].b[0][0], &A.tmb, i0, rs + kGhost, &bar[0]);
+      for (int hc = 0; hc < NSTG - 1 && hc < 2 * nch; ++hc) {  // halves 0..2; half hc+3 is issued in half hc
+        mbar_expect_tx(&bar[hc], kBytes);
+        tma_load_2d(&st[hc].x[0][0], &A.tmx, i0, rs + hc * CR + kGhost, &bar[hc]);
+        tma_load_2d(&st[hc].b[0][0], &A.tmb, i0, rs + hc * CR + kGhost, &bar[hc]);
+      }
     }
     __syncwarp();
     // converged at an earlier iteration: nothing to do.  Tested after the first
     // TMA issue so that the control-word round trip does not delay the item's
     // first chunk; the loads in flight are waited for before leaving.
     if (*(volatile int *)&A.ctl->k_done >= 0) {
-      mbar_wait_warp(&bar[0], 0);
+      for (int hc = 0; hc < NSTG - 1 && hc < 2 * nch; ++hc) mbar_wait_warp(&bar[hc], 0);
       return;
     }
     bool lane_own[NS];
@@ -419,34 +441,42 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
     irr0 = __reduce_min_sync(FULL, irr0);
     irr1 = __reduce_max_sync(FULL, irr1);
     for (int c = 0; c < nch; ++c) {
-      const int s = c & 1;
+      const int hA = 2 * c, hB = hA + 1;  // this window's halves
       const int rb = rs + c * W;
       const bool fast = rb + W - 2 < irr0 || rb - 2 * WM > irr1;
       const bool hasf = boxstrip && rb + W - 2 >= A.box.j0 && rb - 2 * WM < A.box.j1;
-      mbar_wait_warp(&bar[s], (c >> 1) & 1);
+      mbar_wait_warp(&bar[hA % NSTG], (hA / NSTG) & 1);
       const bool ownall = rb - 2 * WM >= j0 && rb + W - 2 < j1;
-      // after step 0: load chunk c + 1 into the other stage (see wf_nstg; for
-      // c = 0 that stage only supplied the b of the junk row rs - 1)
-      auto refill = [&]() {
+      // refill the stage of half h - 1 with half h + 3 once the first step of half h
+      // has read its last b row (see wf_nstg; for h = 0 that stage only supplied
+      // the b of the junk row rs - 1)
+      auto refill = [&](int h) {
         __syncwarp();
-        if (l == 0 && c + 1 < nch) {
-          mbar_expect_tx(&bar[s ^ 1], kBytes);
-          tma_load_2d(&st[s ^ 1].x[0][0], &A.tmx, i0, rs + (c + 1) * W + kGhost, &bar[s ^ 1]);
-          tma_load_2d(&st[s ^ 1].b[0][0], &A.tmb, i0, rs + (c + 1) * W + kGhost, &bar[s ^ 1]);
+        const int hn = h + NSTG - 1;
+        if (l == 0 && hn < 2 * nch) {
+          const int sr = hn % NSTG;
+          mbar_expect_tx(&bar[sr], kBytes);
+          tma_load_2d(&st[sr].x[0][0], &A.tmx, i0, rs + hn * CR + kGhost, &bar[sr]);
+          tma_load_2d(&st[sr].b[0][0], &A.tmb, i0, rs + hn * CR + kGhost, &bar[sr]);
         }
       };
+      struct {
+        decltype(refill) &rf;
+        unsigned long long *bar;
+        int hA, hB;
+        __device__ void after_first() { rf(hA); }
+        __device__ void wait_second() { mbar_wait_warp(&bar[hB % NSTG], (hB / NSTG) & 1); }
+        __device__ void after_second() { rf(hB); }
+      } hooks{refill, bar, hA, hB};
+      const WfStage<WM> &SA = st[hA % NSTG], &SB = st[hB % NSTG], &Sp = st[(hA + NSTG - 1) % NSTG];
       if (fast && interior && ownall)
-        wf_chunk<WM, TP, 2, true, APX>(X, B, st[s], st[s ^ 1], C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax,
-                                       refill);
+        wf_chunk<WM, TP, 2, true, APX>(X, B, SA, SB, Sp, C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax, hooks);
       else if (fast && interior)
-        wf_chunk<WM, TP, 2, false, APX>(X, B, st[s], st[s ^ 1], C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax,
-                                        refill);
+        wf_chunk<WM, TP, 2, false, APX>(X, B, SA, SB, Sp, C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax, hooks);
       else if (fast)
-        wf_chunk<WM, TP, 1, false, APX>(X, B, st[s], st[s ^ 1], C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax,
-                                        refill);
+        wf_chunk<WM, TP, 1, false, APX>(X, B, SA, SB, Sp, C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax, hooks);
       else
-        wf_chunk<WM, TP, 0, false, APX>(X, B, st[s], st[s ^ 1], C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax,
-                                        refill);
+        wf_chunk<WM, TP, 0, false, APX>(X, B, SA, SB, Sp, C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax, hooks);
     }
   }
   // residual of each fused iteration: warp -> CTA -> atomicMax on its bit pattern
@@ -687,7 +717,15 @@ __global__ void __launch_bounds__(32, wf4_min_blocks<WM>()) k_sor_wf4(const __gr
   const int item = blockIdx.x;
   const Geo &g = A.g;
   int sx = item / A.segs, sy = item % A.segs;  // strip-major item order
-  if (A.order == 0) {
+  if (A.seg_mode == 1) {  // edge / interior subsets (decomposed grids), as in k_sor_wf
+    const int ne = A.e_lo + A.e_hi, k = item % ne;
+    sx = item / ne;
+    sy = k < A.e_lo ? k : A.segs - A.e_hi + (k - A.e_lo);
+  } else if (A.seg_mode == 2) {
+    const int ni_ = A.segs - A.e_lo - A.e_hi;
+    sx = item / ni_;
+    sy = A.e_lo + item % ni_;
+  } else if (A.order == 0) {
     sx = item % A.strips;
     sy = item / A.strips;
   }
@@ -856,7 +894,7 @@ int wf_cpl() {
   }();
   return cpl;
 }
-int wf_box_rows(int m) { return wf_cpl() == 4 ? m + 1 : 2 * m + 2; }
+int wf_box_rows(int m) { return m + 1; }  // half a window (both layouts)
 #ifdef WF_EXACT
 bool wf_approx() { return false; }
 #else
@@ -936,6 +974,19 @@ void wf_plan(WfArgs &a, int m, int L_force) {
   a.L = L;
   a.segs = (a.g.nj + L - 1) / L;
   a.items = a.strips * a.segs;
+  // edge segments: streamed rows [j0 - 2m, j1 + 2m) leave the owned rows
+  a.seg_mode = 0;
+  a.e_lo = 0;
+  a.e_hi = 0;
+  for (int sy = 0; sy < a.segs; ++sy) {
+    const int j0 = sy * L, j1 = std::min(j0 + L, a.g.nj);
+    const bool edge = j0 - 2 * m < 0 || j1 + 2 * m > a.g.nj;
+    if (edge && sy == a.e_lo) ++a.e_lo;
+  }
+  for (int sy = a.segs - 1; sy >= a.e_lo; --sy) {
+    const int j0 = sy * L, j1 = std::min(j0 + L, a.g.nj);
+    if (j0 - 2 * m < 0 || j1 + 2 * m > a.g.nj) ++a.e_hi; else break;
+  }
   a.order = 2;
   if (const char *e = std::getenv("IBM_WF_ORDER")) a.order = std::atoi(e);
   a.order_g = 8;
