@@ -610,7 +610,7 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
     if (c.wf_L == 0 && !std::getenv("IBM_WF_ROWS")) {
       cand = wf_candidates(c.sl[0].gp, c.wf_m);
       if (cand.size() > 1)
-        tune_n = std::min(2 * (int)cand.size(), 6);
+        tune_n = std::min(2 * (int)cand.size(), 12);  // each candidate twice
       else
         c.wf_L = cand[0];
     }

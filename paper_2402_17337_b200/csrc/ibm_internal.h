@@ -120,6 +120,7 @@ struct TbArgs {
   const double *cE, *cW, *cD, *cN, *cS;
   int ui0, ui1, uj0, uj1;
   int tx, ty, ntx, nty, m;
+  int rc;               // 1: reciprocal diagonals stored in shared memory, 0: recomputed per update
   int s0;               // buffer holding the initial iterate
   double omega, tol;
   int maxit, check_every;
@@ -179,7 +180,7 @@ struct Ctx {
   int wf_L;         // fused-pass segment length chosen by the online tuner (0: not yet)
   int tb_m;         // iterations per grid barrier of the resident mid-grid solve (0: not used)
   TbArgs tb;        // its tile plan (built at init)
-  cudaEvent_t tev[12];  // tuner: start / stop of the first fused passes of a run
+  cudaEvent_t tev[24];  // tuner: start / stop of the first fused passes of a run (12 passes)
   int launches;     // kernels launched in the current step
   cudaEvent_t ev[8];
   void *nccl;      // ncclComm_t when nranks > 1 and !loopback

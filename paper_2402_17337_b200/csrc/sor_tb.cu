@@ -45,7 +45,9 @@ struct TbLayout {  // byte offsets of the shared-memory arrays of one tile regio
   size_t x, b, rc, fl, rp, cE, cW, cD, cN, cS, red, total;
 };
 
-__host__ __device__ inline TbLayout tb_layout(int tx, int ty, int M) {
+// rc: the reciprocal diagonals are stored per cell (25 B per region cell) or, for
+// regions too large for that, recomputed at every update (17 B per cell)
+__host__ __device__ inline TbLayout tb_layout(int tx, int ty, int M, bool rc = true) {
   TbLayout L;
   L.RX = tx + 4 * M;
   L.RY = ty + 4 * M;
@@ -53,7 +55,7 @@ __host__ __device__ inline TbLayout tb_layout(int tx, int ty, int M) {
   size_t o = 0;
   L.x = o;  o += n * 8;
   L.b = o;  o += n * 8;
-  L.rc = o; o += n * 8;
+  L.rc = o; o += rc ? n * 8 : 0;
   L.cE = o; o += (size_t)L.RX * 8;
   L.cW = o; o += (size_t)L.RX * 8;
   L.cD = o; o += (size_t)L.RX * 8;
@@ -102,9 +104,9 @@ __device__ __forceinline__ int tb_ix(int x, int y) { return y * TB_RX + ((x & 1)
 // counted), so only x = 0 / 63 (lane 0 with e = 0, lane 31 with e = 1) are
 // skipped.  Rows whose 64 cells are all updated with open faces (rp) take the
 // flag-free path.  RES: fold |d| of owned cells into t.
-template <bool RES>
+template <bool RES, bool RC>
 __device__ __forceinline__ void tb_half(const TbCtx &T, int h, int M, double omega, const double (&cE2)[2],
-                                        const double (&cW2)[2], unsigned long long &t) {
+                                        const double (&cW2)[2], const double (&cD2)[2], unsigned long long &t) {
   constexpr int R = TB_R;  // rows per pass of a warp: their loads are issued before any store (ILP)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int y0 = h + 1, y1 = T.RY - 2 - h;
@@ -112,10 +114,10 @@ __device__ __forceinline__ void tb_half(const TbCtx &T, int h, int M, double ome
   const int e = (T.gi0 + T.gj0 + T.jl0 + (h & 1) + y0 + w) & 1;
   const bool act = e ? lane != 31 : lane != 0;
   const bool lres = RES && lane >= H / 2 && lane < 32 - H / 2;  // owned columns (x in [H, 64-H))
-  const double cE = e ? cE2[1] : cE2[0], cW = e ? cW2[1] : cW2[0];
+  const double cE = e ? cE2[1] : cE2[0], cW = e ? cW2[1] : cW2[0], cD = e ? cD2[1] : cD2[0];
   const int offC = (e << 5) + lane, offO = ((e ^ 1) << 5) + lane + e;  // cell; east neighbour (west = -1)
   for (int yb = y0 + w; yb <= y1; yb += TBW * R) {
-    double xo[R], nm[R];
+    double xo[R], nm[R], rcp[R];
     bool upd[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -132,6 +134,10 @@ __device__ __forceinline__ void tb_half(const TbCtx &T, int h, int M, double ome
         aS = (f & PF_S) ? 0.0 : aS;
       }
       upd[r] = u;
+      if (RC)
+        rcp[r] = T.rc[iC];
+      else  // the same IEEE operations as the stored reciprocal (setup below)
+        rcp[r] = __drcp_rn(((aE + aW) + (aN + aS)) + cD);
       xo[r] = T.x[iC];
       nm[r] = __fma_rn(aN, T.x[iC + TB_RX],
                        __fma_rn(aE, T.x[iE], __fma_rn(aW, T.x[iE - 1], __fma_rn(aS, T.x[iC - TB_RX], T.b[iC]))));
@@ -140,7 +146,7 @@ __device__ __forceinline__ void tb_half(const TbCtx &T, int h, int M, double ome
     for (int r = 0; r < R; ++r) {
       const int y = min(yb + r * TBW, y1);
       const int iC = y * TB_RX + offC;
-      const double d = __fma_rn(nm[r], T.rc[iC], -xo[r]);
+      const double d = __fma_rn(nm[r], rcp[r], -xo[r]);
       if (upd[r]) {
         T.x[iC] = __fma_rn(omega, d, xo[r]);
         if (RES && lres && y >= H && y < T.RY - H) t = umax64(t, abs_bits(d));
@@ -185,12 +191,12 @@ __device__ __forceinline__ void tb_store_x(const TbCtx &T, double *__restrict__ 
   }
 }
 
-template <int M>
+template <int M, bool RC>
 __global__ void __launch_bounds__(TBT, 2) k_sor_tb(const __grid_constant__ TbArgs A) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char smraw[];
-  const TbLayout L = tb_layout(A.tx, A.ty, M);
+  const TbLayout L = tb_layout(A.tx, A.ty, M, RC);
   TbCtx T;
   T.x = reinterpret_cast<double *>(smraw + L.x);
   T.b = reinterpret_cast<double *>(smraw + L.b);
@@ -251,19 +257,20 @@ __global__ void __launch_bounds__(TBT, 2) k_sor_tb(const __grid_constant__ TbArg
       }
       const int si = tb_ix(x, y);
       T.b[si] = bb;
-      T.rc[si] = rc;
+      if (RC) T.rc[si] = rc;
       T.fl[si] = f;
     }
   }
 
   // column coefficients of the lane's two columns (registers for the whole solve)
-  double cE2[2], cW2[2];
+  double cE2[2], cW2[2], cD2[2];
   {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     __syncthreads();
     for (int e = 0; e < 2; ++e) {
       cE2[e] = T.cE[2 * lane + e];
       cW2[e] = T.cW[2 * lane + e];
+      cD2[e] = T.cD[2 * lane + e];
     }
     for (int y = w; y < T.RY; y += TBW) {  // rows without flags to apply
       const bool plain = T.fl[tb_ix(2 * lane, y)] == TB_UPD && T.fl[tb_ix(2 * lane + 1, y)] == TB_UPD;
@@ -281,7 +288,7 @@ __global__ void __launch_bounds__(TBT, 2) k_sor_tb(const __grid_constant__ TbArg
     unsigned long long t[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
     for (int h = 0; h < 2 * M; ++h) {
-      tb_half<true>(T, h, M, A.omega, cE2, cW2, t[h >> 1]);
+      tb_half<true, RC>(T, h, M, A.omega, cE2, cW2, cD2, t[h >> 1]);
       __syncthreads();
     }
     tb_store_x(T, A.xb[bin ^ 1], g, M);
@@ -330,7 +337,7 @@ __global__ void __launch_bounds__(TBT, 2) k_sor_tb(const __grid_constant__ TbArg
       __syncthreads();
       unsigned long long dummy = 0ull;
       for (int h = 0; h < 2 * (stop + 1); ++h) {
-        tb_half<false>(T, h, M, A.omega, cE2, cW2, dummy);
+        tb_half<false, RC>(T, h, M, A.omega, cE2, cW2, cD2, dummy);
         __syncthreads();
       }
       tb_store_x(T, A.xb[bin ^ 1], g, M);
@@ -345,22 +352,30 @@ __global__ void __launch_bounds__(TBT, 2) k_sor_tb(const __grid_constant__ TbArg
   }
 }
 
-template <int M>
-bool tb_fits_m(const TbArgs &a, int *per_sm) {
-  const TbLayout L = tb_layout(a.tx, a.ty, M);
+template <int M, bool RC>
+bool tb_fits_mr(const TbArgs &a, int *per_sm) {
+  const TbLayout L = tb_layout(a.tx, a.ty, M, RC);
   if (L.total > 227 * 1024) return false;
-  cudaFuncSetAttribute(k_sor_tb<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+  cudaFuncSetAttribute(k_sor_tb<M, RC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   int per = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sor_tb<M>, TBT, L.total) != cudaSuccess) return false;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sor_tb<M, RC>, TBT, L.total) != cudaSuccess) return false;
   *per_sm = per;
   return per >= 1;
 }
+template <int M>
+bool tb_fits_m(const TbArgs &a, int *per_sm) {
+  return a.rc ? tb_fits_mr<M, true>(a, per_sm) : tb_fits_mr<M, false>(a, per_sm);
+}
 
+template <int M, bool RC>
+cudaError_t tb_launch_mr(const TbArgs &a, cudaStream_t st) {
+  const TbLayout L = tb_layout(a.tx, a.ty, M, RC);
+  void *args[] = {const_cast<TbArgs *>(&a)};
+  return cudaLaunchCooperativeKernel((void *)k_sor_tb<M, RC>, dim3(a.ntx * a.nty), dim3(TBT), args, L.total, st);
+}
 template <int M>
 cudaError_t tb_launch_m(const TbArgs &a, cudaStream_t st) {
-  const TbLayout L = tb_layout(a.tx, a.ty, M);
-  void *args[] = {const_cast<TbArgs *>(&a)};
-  return cudaLaunchCooperativeKernel((void *)k_sor_tb<M>, dim3(a.ntx * a.nty), dim3(TBT), args, L.total, st);
+  return a.rc ? tb_launch_mr<M, true>(a, st) : tb_launch_mr<M, false>(a, st);
 }
 
 }  // namespace
@@ -373,7 +388,9 @@ bool tb_plan(TbArgs &a, int nx, int nj, int M, int sms) {
   a.m = M;
   const int tx = TB_RX - 4 * M;
   const int ntx = (nx + tx - 1) / tx;
-  for (int per = 2; per >= 1; --per) {
+  for (int variant = 0; variant < 4; ++variant) {  // (rc stored, 2/SM), (stored, 1), (recomputed, 2), (recomputed, 1)
+    const int per = 2 - (variant & 1);
+    const bool rc = variant < 2;
     const int cap = per * sms;
     if (ntx > cap) continue;
     const int nty0 = std::max(1, std::min(cap / ntx, nj / 8));  // tiles of >= 8 owned rows
@@ -383,7 +400,8 @@ bool tb_plan(TbArgs &a, int nx, int nj, int M, int sms) {
     b.ty = ty;
     b.ntx = ntx;
     b.nty = nty;
-    const TbLayout L = tb_layout(tx, ty, M);
+    b.rc = rc ? 1 : 0;
+    const TbLayout L = tb_layout(tx, ty, M, rc);
     if (L.total * per > 227 * 1024) continue;
     int got = 0;
     const bool ok = (M == 2) ? tb_fits_m<2>(b, &got) : (M == 3) ? tb_fits_m<3>(b, &got) : tb_fits_m<4>(b, &got);

@@ -144,9 +144,24 @@ __device__ __forceinline__ void wf_nb(const double2 (&X)[NS][W], double (&nb)[NS
 // 32 bits only (LOP3 + VIMNMX, which ptxas fuses pairwise into VIMNMX3); the pass
 // then reports a lower bound LB = H << 32 <= rho, so a stop is only provisional
 // and the host replays that pass with the exact one-iteration kernel (sor_solve).
+#ifndef WF_RES2
+#define WF_RES2 1
+#endif
 template <bool APX>
 __device__ __forceinline__ void wf_acc(unsigned long long &t, double d, unsigned m) {
-  if (APX) {
+  if (APX && WF_RES2) {
+    // Two accumulators in the halves of t, no sign clear: lo = signed max of the
+    // high words (the largest positive d), hi = unsigned max (the largest-magnitude
+    // negative d if there is one, else the largest positive); the magnitude bound
+    // is max(lo, hi & 0x7fffffff) (wf_res_word).  One VIMNMX per node each, fused
+    // pairwise into VIMNMX3, and no LOP3 where m is the constant all-ones mask.
+    unsigned lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "d"(d));
+    hi &= m;
+    const unsigned tp = (unsigned)max((int)(unsigned)t, (int)hi);
+    const unsigned tn = max((unsigned)(t >> 32), hi);
+    t = ((unsigned long long)tn << 32) | tp;
+  } else if (APX) {
     unsigned lo, hi;
     asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "d"(d));
     hi &= 0x7fffffffu & m;
@@ -155,6 +170,13 @@ __device__ __forceinline__ void wf_acc(unsigned long long &t, double d, unsigned
     const unsigned long long e = abs_bits_masked(d, m);
     t = e > t ? e : t;
   }
+}
+// comparable residual word of an accumulator: APX -> the high word H of max|d|
+// (LB = H << 32 is a lower bound of rho), exact -> the bit pattern of max|d|
+template <bool APX>
+__device__ __forceinline__ unsigned long long wf_res_word(unsigned long long t) {
+  if (APX && WF_RES2) return (unsigned long long)max((unsigned)t, (unsigned)(t >> 32) & 0x7fffffffu);
+  return t;
 }
 
 // okm: all ones if the row is owned by the item, else 0 (an integer mask, not a
@@ -487,7 +509,7 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       const int p = l + 32 * s;
-      if (p >= WM && p <= 32 * NS - 1 - WM) t = umax64(t, tmax[i][s]);
+      if (p >= WM && p <= 32 * NS - 1 - WM) t = umax64(t, wf_res_word<APX>(tmax[i][s]));
     }
 #pragma unroll
     for (int off = 16; off; off >>= 1) t = umax64(t, __shfl_xor_sync(FULL, t, off));
@@ -815,7 +837,7 @@ __global__ void __launch_bounds__(32, wf4_min_blocks<WM>()) k_sor_wf4(const __gr
     unsigned long long t = 0ull;
 #pragma unroll
     for (int s = 0; s < 2; ++s)
-      if (2 * l + s >= WM && 2 * l + s <= SC4 / 2 - 1 - WM) t = umax64(t, tmax[i][s]);
+      if (2 * l + s >= WM && 2 * l + s <= SC4 / 2 - 1 - WM) t = umax64(t, wf_res_word<APX>(tmax[i][s]));
 #pragma unroll
     for (int off = 16; off; off >>= 1) t = umax64(t, __shfl_xor_sync(FULL, t, off));
     if (l == 0 && t) atomicMax(&A.rho_bits[A.k + i], APX ? t << 32 : t);  // APX: LB = H << 32
@@ -959,6 +981,9 @@ std::vector<int> wf_candidates(const Geo &g, int m) {
   std::vector<int> c{L0};
   if (L0 / 2 >= wf_rows_min(m)) c.push_back(L0 / 2);
   if (2 * L0 <= 512 && (long)strips * ((g.nj + 2 * L0 - 1) / (2 * L0)) >= wf_items_target()) c.push_back(2 * L0);
+  // (Wave-filling lengths -- L with items / warp slots just below an integer, e.g.
+  // 140, 222, 284, 374 at 8192^2 -- were measured slower, 0.123-0.151 vs 0.113 ms per
+  // iteration: the DRAM pattern of the concurrently streamed rows favours L = 2^k.)
   return c;
 }
 

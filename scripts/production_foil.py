@@ -90,6 +90,20 @@ def main():
         cfg, S, r = run_level(lv, args.steps, chunk=args.chunk, **kw)
         r["omega_p"] = cfg.omega_p
         r["maxit_p"] = cfg.maxit_p
+        # plunge-cycle statistics (period 2 pi / k): cycle means, amplitude and the
+        # rms change of the c_l history from one cycle to the next (SURVEY §8(c) force pins)
+        T = 2 * np.pi / cfg.body.k
+        per = int(round(T / cfg.dt))
+        cyc = []
+        for c0 in range(0, len(S) - per + 1, per):
+            cl, cd = S[c0:c0 + per, 6], S[c0:c0 + per, 5]
+            d = {"cycle": c0 // per + 1, "cl_mean": float(cl.mean()), "cd_mean": float(cd.mean()),
+                 "cl_amplitude": float(0.5 * (cl.max() - cl.min()))}
+            if c0 >= per:
+                prev = S[c0 - per:c0, 6]
+                d["cl_rms_change_vs_previous"] = float(np.sqrt(np.mean((cl - prev) ** 2)) / np.sqrt(np.mean(cl ** 2)))
+            cyc.append(d)
+        r["cycles"] = cyc
         res["levels"].append(r)
         np.savetxt("%s_M%d.csv" % (args.out, lv), np.c_[S[:, 0], S[:, 5], S[:, 6], S[:, 1], S[:, 2]],
                    delimiter=",", header="t_bar,cd,cl,it_uv,it_p", comments="")

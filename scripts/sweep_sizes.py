@@ -21,7 +21,7 @@ import ibm_inputs as I  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_sweep.json"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02_sweep.json"))
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--sizes", default="256,512,1024,2048,4096,8192")
     args = ap.parse_args()
@@ -58,7 +58,9 @@ def main():
         rows.append({"n": n, "dt": cfg.dt, "updates_per_s": upd / (ms / 1e3), "ms_per_step": ms / args.steps,
                      "it_p": stats[:, 2].tolist(), "it_uv": stats[:, 1].tolist(),
                      "poisson_ms_per_iteration_200": it_ms, "poisson_GBs": gbs, "frac_of_peak": gbs / peak,
-                     "working_set_MB": g.ws.numel() / 1e6})
+                     "working_set_MB": g.ws.numel() / 1e6,
+                     "poisson_path": ("k_sor_wf<%d> fused pass" % g.query("wf_m")) if g.query("wf_m") > 1 else
+                     ("k_sor_tb<%d> resident solve" % g.query("tb_m")) if g.query("tb_m") else "k_sor one-iteration pass"})
         print(json.dumps(rows[-1]), flush=True)
         g.close()
         del g
