@@ -360,7 +360,9 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
   for (int i = 0; i < WM; ++i)
 #pragma unroll
     for (int s = 0; s < NS; ++s) tmax[i][s] = 0ull;
-  const int item = blockIdx.x * WNW + w;
+  // (one warp per CTA: the item is blockIdx.x, provably warp-uniform, so the TMA
+  // coordinates below live in uniform registers)
+  const int item = WNW == 1 ? (int)blockIdx.x : (int)blockIdx.x * WNW + w;
   if (item >= A.items && *(volatile int *)&A.ctl->k_done >= 0) return;  // (working warps: below)
   if (item < A.items) {
     const Geo &g = A.g;
@@ -397,13 +399,11 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
     if (l == 0) {
       for (int s = 0; s < NSTG; ++s) mbar_init(&bar[s], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      for (int hc = 0; hc < NSTG - 1 && hc < 2 * nch; ++hc) {  // halves 0..2; half hc+3 is issued in half hc
-        mbar_expect_tx(&bar[hc], kBytes);
-        tma_load_2d(&st[hc].x[0][0], &A.tmx, i0, rs + hc * CR + kGhost, &bar[hc]);
-        tma_load_2d(&st[hc].b[0][0], &A.tmb, i0, rs + hc * CR + kGhost, &bar[hc]);
-      }
     }
     __syncwarp();
+    for (int hc = 0; hc < NSTG - 1 && hc < 2 * nch; ++hc)  // halves 0..2; half hc+3 is issued in half hc
+      tma_load_pair_elect(&bar[hc], kBytes, &st[hc].x[0][0], &A.tmx, &st[hc].b[0][0], &A.tmb, i0,
+                          rs + hc * CR + kGhost);
     // converged at an earlier iteration: nothing to do.  Tested after the first
     // TMA issue so that the control-word round trip does not delay the item's
     // first chunk; the loads in flight are waited for before leaving.
@@ -475,11 +475,10 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
       auto refill = [&](int h) {
         __syncwarp();
         const int hn = h + NSTG - 1;
-        if (l == 0 && hn < 2 * nch) {
+        if (hn < 2 * nch) {  // (warp-uniform)
           const int sr = hn % NSTG;
-          mbar_expect_tx(&bar[sr], kBytes);
-          tma_load_2d(&st[sr].x[0][0], &A.tmx, i0, rs + hn * CR + kGhost, &bar[sr]);
-          tma_load_2d(&st[sr].b[0][0], &A.tmb, i0, rs + hn * CR + kGhost, &bar[sr]);
+          tma_load_pair_elect(&bar[sr], kBytes, &st[sr].x[0][0], &A.tmx, &st[sr].b[0][0], &A.tmb, i0,
+                              rs + hn * CR + kGhost);
         }
       };
       struct {

@@ -17,7 +17,10 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libibm_b200.so")
+# (IBM_LIB_VARIANT=name loads libibm_b200_<name>.so: kernel tuning experiments only,
+# built by scripts/build_variants.py)
+LIB_PATH = os.path.join(HERE, "libibm_b200%s.so" % (("_" + os.environ["IBM_LIB_VARIANT"])
+                                                    if os.environ.get("IBM_LIB_VARIANT") else ""))
 
 IBM_OK, IBM_WARN_NOCONV, IBM_ERR_CONFIG, IBM_ERR_DIVERGED = 0, 1, 2, 3
 IBM_ERR_ARG, IBM_ERR_CUDA, IBM_ERR_NCCL, IBM_ERR_STATE = 4, 5, 6, 7
