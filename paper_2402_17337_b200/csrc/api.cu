@@ -429,6 +429,30 @@ int refresh_time(Ctx &c) {
 // CTA takes the convergence decision on the device; if it stops at an iteration
 // inside a fused pass, that pass is replayed from its (intact) input buffer up to
 // the decided iteration.  *buf_out receives the buffer index of the result.
+// The fused pass's per-segment table (WfSeg) for slab r at the plan's segment
+// length: built on the host from the row coefficients once per (slab, L) and
+// uploaded on the solver stream; kept until ibm_destroy.
+int wf_attach_seg(Ctx &c, size_t r, WfArgs &wa) {
+  const long key = (long)r * 1000000L + wa.L;
+  auto it = c.wf_segs.find(key);
+  if (it == c.wf_segs.end()) {
+    std::vector<WfSeg> tab = wf_seg_table(wa, c.wf_m, c.h_cNp.data(), c.h_cSp.data());
+    WfSeg *d = nullptr;
+    if (cudaMalloc(&d, tab.size() * sizeof(WfSeg)) != cudaSuccess) {
+      c.err = "cudaMalloc (fused-pass segment table)";
+      return IBM_ERR_CUDA;
+    }
+    it = c.wf_segs.emplace(key, std::make_pair(std::move(tab), d)).first;
+    if (cudaMemcpyAsync(d, it->second.first.data(), it->second.first.size() * sizeof(WfSeg),
+                        cudaMemcpyHostToDevice, c.stream) != cudaSuccess) {
+      c.err = "cudaMemcpyAsync (fused-pass segment table)";
+      return IBM_ERR_CUDA;
+    }
+  }
+  wa.seg = it->second.second;
+  return IBM_OK;
+}
+
 int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *status, int iters_override,
               int *buf_out) {
   const ibm_config &cfg = c.cfg;
@@ -549,6 +573,7 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
     wa.rho_bits = c.rho_bits; wa.ctl = c.ctl;
     wa.multi = mult ? 1 : 0;
     wf_plan(wa, c.wf_m);
+    if (int e = wf_attach_seg(c, r, wa)) return e;
   }
   // decomposed fused passes: an exchange of the last pass's output may be in
   // flight on the comm stream; the main stream joins it before touching ghost rows
@@ -614,7 +639,10 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
       else
         c.wf_L = cand[0];
     }
-    if (c.wf_L > 0) wf_plan(was[0], c.wf_m, c.wf_L);
+    if (c.wf_L > 0) {
+      wf_plan(was[0], c.wf_m, c.wf_L);
+      if (int e = wf_attach_seg(c, 0, was[0])) return e;
+    }
   }
   for (;;) {
     const int kend = std::min(maxit, k + batch - 1);
@@ -660,6 +688,7 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
         const bool tuning = tune_launched < tune_n;
         if (tuning) {
           wf_plan(was[0], c.wf_m, cand[tune_launched % cand.size()]);
+          if (int e = wf_attach_seg(c, 0, was[0])) return e;
           CK(cudaEventRecord(c.tev[2 * tune_launched], c.stream));
         }
         for (size_t r = 0; r < c.sl.size(); ++r) {
@@ -702,6 +731,7 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
         }
         c.wf_L = cand[std::min_element(best.begin(), best.end()) - best.begin()];
         wf_plan(was[0], c.wf_m, c.wf_L);
+        if (int e = wf_attach_seg(c, 0, was[0])) return e;
       }
       tune_n = 0;
     }
@@ -1035,6 +1065,8 @@ int ibm_init(const ibm_config *cfg, void *d_workspace, size_t bytes, void *cuda_
     }
   }
   HostMetric h = host_metric(*cfg);
+  c.h_cNp = h.cNp;
+  c.h_cSp = h.cSp;
   c.h_xn = nullptr;
   c.h_yn = nullptr;
   auto up = [&](double *d, const std::vector<double> &v) {
@@ -1289,6 +1321,7 @@ int ibm_destroy(ibm_ctx *ctx) {
   cudaFreeHost(c.h_ctl);
   cudaFreeHost(c.h_red);
   cudaFreeHost(c.h_nan);
+  for (auto &kv : c.wf_segs) cudaFree(kv.second.second);
   delete[] c.h_xn;
   delete[] c.h_yn;
   delete ctx;

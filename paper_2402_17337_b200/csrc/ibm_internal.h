@@ -8,6 +8,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <string>
+#include <map>
 #include <vector>
 
 #include <cuda.h>  // CUtensorMap (TMA descriptors); no libcuda link
@@ -85,6 +86,15 @@ struct SorArgs {
 // Temporally blocked Poisson pass (sor_wf.cu): WM red-black iterations per HBM
 // pass.  One warp = one work item = a strip of 64 stored columns (64 - 4 WM
 // owned) x a segment of L owned rows, streamed top to bottom.
+// Per-segment data of the fused pass (host-built for each slab and segment
+// length, wf_seg_table): the segment's reference row coefficients and the range
+// [irr0, irr1] of its streamed local rows that are irregular apart from the body
+// box -- outside the family's updatable rows or with other row coefficients
+// (irr0 > irr1: none).
+struct WfSeg {
+  double cN0, cS0;
+  int irr0, irr1;
+};
 struct WfArgs {
   CUtensorMap tmx;      // iterate, box 64 x (2 WM + 2) rows
   CUtensorMap tmb;      // right-hand side, same box
@@ -105,6 +115,7 @@ struct WfArgs {
   int k, maxit, check_every;
   unsigned long long *rho_bits;
   SorCtl *ctl;
+  const WfSeg *seg;     // [segs] (wf_seg_table for this slab and L)
 };
 constexpr int kWfMaxM = 4;  // fused iterations per pass: 2..kWfMaxM instantiated
 
@@ -178,6 +189,8 @@ struct Ctx {
   int hint_uv, hint_p;
   int wf_m;         // Poisson iterations fused per HBM pass (1 = unfused k_sor)
   int wf_L;         // fused-pass segment length chosen by the online tuner (0: not yet)
+  std::vector<double> h_cNp, h_cSp;  // host row coefficients of the p family (wf_seg_table)
+  std::map<long, std::pair<std::vector<WfSeg>, WfSeg *>> wf_segs;  // (slab, L) -> host / device table
   int tb_m;         // iterations per grid barrier of the resident mid-grid solve (0: not used)
   TbArgs tb;        // its tile plan (built at init)
   cudaEvent_t tev[24];  // tuner: start / stop of the first fused passes of a run (12 passes)
@@ -204,13 +217,15 @@ constexpr int kSorBoxW = 64, kSorBoxHx = 20, kSorBoxHb = 18;
 constexpr int kSorTileX = 60, kSorTileY = 16;
 void launch_sor_iteration(const SorArgs &a, cudaStream_t st, int grid);
 // temporally blocked Poisson pass: rows of the TMA box, segment length, launch
-int wf_cpl();  // columns per lane of the fused pass: 2 (64-column strips) or 4 (128)
+int wf_lag();  // half-sweep lag of the fused pass (1 or 2; sor_wf.cu)
 int wf_box_rows(int m);
 bool wf_approx();  // the fused pass reports high-word residual bounds (stops are provisional)
 int wf_box_cols();
 void wf_plan(WfArgs &a, int m, int L_force = 0);
 // segment lengths worth trying for this slab (the static choice first)
 std::vector<int> wf_candidates(const Geo &g, int m);
+// WfSeg of every segment of a plan (a.g, a.L, a.segs, a.uj0/uj1) from the host row coefficients
+std::vector<WfSeg> wf_seg_table(const WfArgs &a, int m, const double *cN, const double *cS);
 bool wf_viable(int ni, int nj, int m);
 cudaError_t launch_sor_wf(const WfArgs &a, int m, cudaStream_t st);
 void launch_sor_check(SorCtl *ctl, const unsigned long long *rho_bits, int k, int maxit, int check_every,

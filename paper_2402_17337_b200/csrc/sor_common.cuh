@@ -91,6 +91,22 @@ __device__ __forceinline__ void tma_load_pair_elect(unsigned long long *bar, uin
       : "memory");
 }
 
+// Same, issued only if `go` (warp-uniform): the predicate is folded into the
+// elected lane's, so there is no branch either.
+__device__ __forceinline__ void tma_load_pair_elect_if(bool go, unsigned long long *bar, uint32_t bytes, void *dx,
+                                                       const CUtensorMap *mx, void *db, const CUtensorMap *mb, int c0,
+                                                       int c1) {
+  asm volatile(
+      "{\n .reg .pred p, q;\n elect.sync _|p, 0xffffffff;\n setp.ne.b32 q, %8, 0;\n and.pred p, p, q;\n"
+      "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
+      "@p cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%2], [%3, {%6, %7}], [%0];\n"
+      "@p cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%4], [%5, {%6, %7}], [%0];\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(bytes), "r"(smem_u32(dx)), "l"(reinterpret_cast<uint64_t>(mx)), "r"(smem_u32(db)),
+      "l"(reinterpret_cast<uint64_t>(mb)), "r"(c0), "r"(c1), "r"((int)go)
+      : "memory");
+}
+
 __device__ __forceinline__ void tma_load_1d(void *dst, const CUtensorMap *map, int c0, unsigned long long *bar) {
   tma_load_2d(dst, map, c0, 0, bar);  // one-row 2-D map
 }

@@ -49,60 +49,58 @@ constexpr unsigned FULL = 0xffffffffu;
 // One warp per CTA (measured, 8192^2 m = 3: 0.134 ms/iteration against 0.145 with
 // 4 warps per CTA): a CTA's resources are released as soon as its one item is
 // done, so slow items (body, edges) do not hold fast ones at the CTA barrier.
-#ifndef WF_NW
-#define WF_NW 1
+constexpr int WNT = 32;
+// Half-sweep lag.  At step q (row rb + q enters the register window) half-sweep
+// h = 0 .. 2WM-1 updates row rb + q - 1 - LAG h.  LAG = 1 is the oracle's sweep
+// order restricted to the strip with every half-sweep one row behind the previous
+// one: inside a step, half-sweep h reads the row half-sweep h-1 has just updated
+// (its north neighbour), a chain of 2WM dependent updates per step.  LAG = 2 keeps
+// the same dependences one step apart -- h at row R reads rows R-1 .. R+1, which
+// h-1 updated in earlier steps (R+1 at step q-1) and h+1 has not touched yet (it
+// reaches R+1 at step q+3) -- so the 2WM updates of a step are independent, at the
+// cost of a deeper window (4WM+1 rows instead of 2WM+2) and 2WM-1 more streamed
+// rows per item.  Both orders give every update the operands of the oracle's order
+// (the same iterate, bit for bit).  Process-wide (the TMA box height depends on
+// it): IBM_WF_LAG overrides WF_LAG_DEFAULT.  Measured (8192^2, m = 3, cold): LAG 2
+// removes most dependency stalls (ncu "wait" 8.1 k -> 2.8-3.5 k samples) but its
+// 84-update chunk bodies miss in the instruction cache (no_instruction 0.5 k ->
+// 3.2-6.8 k) and its 3 stages of 7 rows wait longer for TMA data: 0.143-0.148 ms
+// per iteration against 0.110 for LAG 1, which stays the default.
+#ifndef WF_LAG_DEFAULT
+#define WF_LAG_DEFAULT 1
 #endif
-constexpr int WNW = WF_NW;  // warps per CTA (independent work items)
-constexpr int WNT = 32 * WNW;
-// TMA stages per warp.  A window of W = 2WM+2 rows arrives as two halves of WM+1
-// rows, each in its own stage (4 KB at WM = 3); four stages per warp (the 16 KB of
-// the old two full-window stages).  Half hc is read by its own steps and -- the b
-// of its last row -- by the first step of half hc+1; right after that step (behind
-// a __syncwarp: every lane has consumed the values it read) its stage is refilled
-// with half hc+4.  So no generic-proxy read of a stage is outstanding when the TMA
-// (async proxy) overwrites it -- no cross-proxy write-after-read race and no proxy
-// fence (MEMBAR.ALL.CTA + FENCE.VIEW.ASYNC.S, which would also drain the warp's
-// stores) -- and three halves (3 x 4 - 1 = 11 rows) are in flight ahead of the one
-// being computed (ncu: with one full window of lead, 33 % of the stall samples
-// waited for TMA data).
-#ifndef WF_NSTG
-#define WF_NSTG 4
-#endif
-template <int WM>
-__host__ __device__ constexpr int wf_nstg() {
-  return WF_NSTG;
-}
-// prefetch distance of the four-columns-per-lane kernel below (half windows)
-#ifndef WF_PD
-#define WF_PD 2
-#endif
-constexpr int WPD = WF_PD;
-#ifndef WF_NS
-#define WF_NS 1
-#endif
-constexpr int NS = WF_NS;   // column pairs per lane: lane l holds pairs l + 32 st
-constexpr int SC = 64 * NS;  // stored columns per strip
-#ifndef WF_CPL_DEFAULT
-#define WF_CPL_DEFAULT 2  // columns per lane of the fused pass (wf_cpl)
-#endif
-
-template <int WM>
-struct __align__(128) WfStage {  // half a window: rows rb + h (WM+1) .. + WM
-  double x[WM + 1][SC];
-  double b[WM + 1][SC];
+constexpr int SC = 64;  // stored columns per strip (lane l holds columns 2l, 2l+1)
+template <int WM, int LAG>
+struct WfGeo {
+  static constexpr int DLO = 1 + LAG * (2 * WM - 1);  // last half-sweep's row = entering row - DLO
+  static constexpr int W = (DLO + 2 + 1) & ~1;        // window rows (down to its south neighbour; even)
+  static constexpr int CR = W / 2;                    // rows per TMA stage (half a window)
+  // TMA stages per warp.  Half hc is read by its own steps and -- the b of its
+  // last row -- by the first step of half hc+1; right after that step (behind a
+  // __syncwarp: every lane has consumed the values it read) its stage is refilled
+  // with half hc+NSTG.  So no generic-proxy read of a stage is outstanding when the
+  // TMA (async proxy) overwrites it -- no cross-proxy write-after-read race and no
+  // proxy fence (MEMBAR.ALL.CTA + FENCE.VIEW.ASYNC.S, which would also drain the
+  // warp's stores) -- and NSTG-1 halves are in flight ahead of the one being
+  // computed: 11 rows at LAG 1 (4 stages of 4 KB), 13 at LAG 2 (3 of 7 KB).
+  static constexpr int NSTG = LAG == 1 ? 4 : 3;
 };
-template <int WM>
+template <int CR>
+struct __align__(128) WfStage {  // half a window: CR rows of x and b
+  double x[CR][SC];
+  double b[CR][SC];
+};
+template <int WM, int LAG>
 constexpr size_t wf_smem() {
-  return (size_t)WNW * wf_nstg<WM>() * (sizeof(WfStage<WM>) + sizeof(unsigned long long));
+  using G = WfGeo<WM, LAG>;
+  return (size_t)G::NSTG * (sizeof(WfStage<G::CR>) + sizeof(unsigned long long));
 }
-#ifndef WF_MINB
-#define WF_MINB (8 / WF_NW)  // 8 resident warps per SM (255 registers per thread)
-#endif
-// resident CTAs per SM the register budget is sized for (shared memory permitting)
-template <int WM>
+// 8 resident warps per SM (255 registers per thread), shared memory permitting
+template <int WM, int LAG>
 constexpr int wf_min_blocks() {
-  return (int)((220u * 1024u) / wf_smem<WM>()) < WF_MINB ? (int)((220u * 1024u) / wf_smem<WM>()) : WF_MINB;
+  return (int)((220u * 1024u) / wf_smem<WM, LAG>()) < 8 ? (int)((220u * 1024u) / wf_smem<WM, LAG>()) : 8;
 }
+constexpr int NS = 1;  // column pairs per lane
 
 // Per-lane column data of the columns gi = i0 + 2 (l + 32 st) + e.
 struct WfCols {
@@ -286,27 +284,27 @@ __device__ __forceinline__ void sfor(F &&f) {
 // Stage use: the chunk reads its two half-window stages SA, SB and, at step 0, the b row rb-1 from
 // the previous half's stage Sp; the hooks wait for the second half's stage and
 // refill a stage once it is no longer read (see wf_nstg).
-template <int WM, int TP, int MODE, bool OWN, bool APX, class Hooks>
-__device__ __forceinline__ void wf_chunk(double2 (&X)[NS][2 * WM + 2], double2 (&B)[NS][2 * WM + 2],
-                                         const WfStage<WM> &SA, const WfStage<WM> &SB, const WfStage<WM> &Sp,
-                                         const WfCols &C, const WfArgs &A, int rb, int j0, int j1, int i0,
-                                         const bool (&lane_own)[NS], bool hasf, double cN0, double cS0,
-                                         unsigned long long (&tmax)[WM][NS], Hooks &&hooks) {
-  constexpr int W = 2 * WM + 2;
+template <int WM, int LAG, int TP, int MODE, bool OWN, bool APX, class Hooks>
+__device__ __forceinline__ void wf_chunk(double2 (&X)[NS][WfGeo<WM, LAG>::W], double2 (&B)[NS][WfGeo<WM, LAG>::W],
+                                         const WfStage<WfGeo<WM, LAG>::CR> &SA, const WfStage<WfGeo<WM, LAG>::CR> &SB,
+                                         const WfStage<WfGeo<WM, LAG>::CR> &Sp, const WfCols &C, const WfArgs &A,
+                                         int rb, int j0, int j1, int i0, const bool (&lane_own)[NS], bool hasf,
+                                         double cN0, double cS0, unsigned long long (&tmax)[WM][NS], Hooks &&hooks) {
+  using G = WfGeo<WM, LAG>;
+  constexpr int W = G::W, CR = G::CR, DLO = G::DLO;
   const int l = threadIdx.x & 31;
   const double omega = A.omega, omc = A.omc;
   const long pitch = A.g.pitch;
-  // stored row rb + q - 2WM of this lane's first pair (the second is 64 columns on)
-  double *const ob = A.xout + (long)(rb - 2 * WM + kGhost) * pitch + (i0 + 2 * l);
-  constexpr int CR = WM + 1;  // rows per half window (stage)
+  // stored row rb + q - DLO of this lane's pair
+  double *const ob = A.xout + (long)(rb - DLO + kGhost) * pitch + (i0 + 2 * l);
   sfor<W>([&](auto qc) {
     constexpr int q = decltype(qc)::value;
     if constexpr (q == CR) hooks.wait_second();  // second half's stage has landed
     // row rb+q enters the window; the b of row rb+q-1 (first needed in this step)
     // is read now rather than with its x one step earlier (one row less live)
     constexpr int qb = (q + W - 1) % W;
-    const WfStage<WM> &Sx = q < CR ? SA : SB;
-    const WfStage<WM> &Sb = q == 0 ? Sp : (q - 1 < CR ? SA : SB);
+    const WfStage<CR> &Sx = q < CR ? SA : SB;
+    const WfStage<CR> &Sb = q == 0 ? Sp : (q - 1 < CR ? SA : SB);
     constexpr int rx = q % CR, rbb = (q + W - 1) % W % CR;
 #pragma unroll
     for (int st = 0; st < NS; ++st) {
@@ -315,9 +313,9 @@ __device__ __forceinline__ void wf_chunk(double2 (&X)[NS][2 * WM + 2], double2 (
     }
     sfor<2 * WM>([&](auto hc) {
       constexpr int h = decltype(hc)::value;
-      constexpr int Q = ((q - 1 - h) % W + W) % W;  // slot of row rb + q - 1 - h
-      constexpr int E = (TP + Q + h) & 1;           // red (h even): (i + j) even
-      const int r = rb + q - 1 - h;
+      constexpr int Q = ((q - 1 - LAG * h) % W + W) % W;  // slot of row rb + q - 1 - LAG h
+      constexpr int E = (TP + Q + h) & 1;                 // red (h even): (i + j) even
+      const int r = rb + q - 1 - LAG * h;
       [[maybe_unused]] const bool own = OWN || (r >= j0 && r < j1);
       // owned-row mask from the sign bits of r - j0 and j1 - 1 - r (no predicate)
       unsigned okm = 0xffffffffu;
@@ -330,12 +328,12 @@ __device__ __forceinline__ void wf_chunk(double2 (&X)[NS][2 * WM + 2], double2 (
       else
         wf_slow<W, Q, E, APX>(X, B, C, A, r, i0, hasf, omega, omc, own, tmax[h / 2]);
     });
-    // row rb + q - 2WM has received its last half-sweep: store the owned columns
-    const int ro = rb + q - 2 * WM;
+    // row rb + q - DLO has received its last half-sweep: store the owned columns
+    const int ro = rb + q - DLO;
     const bool rowin = OWN || (ro >= j0 && ro < j1);
 #pragma unroll
     for (int st = 0; st < NS; ++st) {
-      const double2 v = X[st][((q - 2 * WM) % W + W) % W];
+      const double2 v = X[st][((q - DLO) % W + W) % W];
       const bool pair_in = MODE == 2 || i0 + 2 * (l + 32 * st) + 1 < A.g.ni;
       st_pred(rowin && lane_own[st] && pair_in, ob + q * pitch + 64 * st, v);
       if (MODE < 2) st_pred1(rowin && lane_own[st] && !pair_in, ob + q * pitch + 64 * st, v.x);
@@ -345,72 +343,102 @@ __device__ __forceinline__ void wf_chunk(double2 (&X)[NS][2 * WM + 2], double2 (
   });
 }
 
-template <int WM, int TP, bool APX>
-__global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __grid_constant__ WfArgs A) {
-  constexpr int W = 2 * WM + 2, OW = SC - 4 * WM, NSTG = wf_nstg<WM>(), CR = WM + 1;
+// Work item (strip sx, segment sy) -> its stored columns and streamed rows.
+struct WfItem {
+  int i0;      // global column of stored column 0
+  int j0, j1;  // owned local rows
+  int rs;      // first streamed row
+  int nch;     // chunks of W rows
+  int sy;      // segment index (WfArgs::seg)
+};
+template <int WM, int LAG>
+__device__ __forceinline__ WfItem wf_item(const WfArgs &A, int item) {
+  constexpr int W = WfGeo<WM, LAG>::W, DLO = WfGeo<WM, LAG>::DLO, OW = SC - 4 * WM;
+  // strip-major item order (consecutive items = the segments of one strip): the
+  // warps streaming at the same time cover ~resident/segs strips over the whole
+  // height; measured 5-6 % faster than segment-row-major at 8192^2 (DRAM
+  // pattern).  IBM_WF_ORDER=0: segment-row-major; 1: scattered rows.
+  int sx = item / A.segs, sy = item % A.segs;
+  if (A.seg_mode == 1) {  // edge segments only (strip-major)
+    const int ne = A.e_lo + A.e_hi, k = item % ne;
+    sx = item / ne;
+    sy = k < A.e_lo ? k : A.segs - A.e_hi + (k - A.e_lo);
+  } else if (A.seg_mode == 2) {  // interior segments only
+    const int ni_ = A.segs - A.e_lo - A.e_hi;
+    sx = item / ni_;
+    sy = A.e_lo + item % ni_;
+  } else if (A.order == 0) {
+    sx = item % A.strips;
+    sy = item / A.strips;
+  } else if (A.order == 1) {
+    sx = item % A.strips;
+    sy = (int)(((long)(item / A.strips) * A.order_mul) % A.segs);
+  } else if (A.order == 3) {  // groups of order_g strips, segment-row-major inside a group
+    const int gsz = A.order_g * A.segs, g0 = (item / gsz) * A.order_g, r = item % gsz;
+    const int gw = min(A.order_g, A.strips - g0);
+    sx = g0 + r % gw;
+    sy = r / gw;
+  }
+  WfItem it;
+  it.i0 = sx * OW - 2 * WM;
+  it.j0 = sy * A.L;
+  it.j1 = min(it.j0 + A.L, A.g.nj);
+  it.rs = it.j0 - 2 * WM;
+  // rows rs .. j1 - 1 + DLO enter the window (row j1 - 1 is stored when j1 - 1 + DLO enters)
+  it.nch = ((it.j1 - it.j0) + 2 * WM + DLO + W - 1) / W;
+  it.sy = sy;
+  return it;
+}
+
+// One warp per CTA; CTA b takes the items b, b + gridDim.x, ... -- one item per
+// CTA by default (gridDim.x = items; wf_persist).  The half-window stage ring runs
+// on across a CTA's items: the refills near the end of an item already stream the
+// first halves of the next one.  The per-item setup is one load of its segment's
+// row data (WfArgs::seg, host-built) plus the lane's column coefficients.
+template <int WM, int LAG, int TP, bool APX>
+__global__ void __launch_bounds__(32, (wf_min_blocks<WM, LAG>())) k_sor_wf(const __grid_constant__ WfArgs A) {
+  using Gm = WfGeo<WM, LAG>;
+  constexpr int W = Gm::W, NSTG = Gm::NSTG, CR = Gm::CR, DLO = Gm::DLO;
   constexpr unsigned kBytes = 2u * CR * SC * 8;  // one half window of x and b
   extern __shared__ __align__(1024) unsigned char smraw[];
-  __shared__ unsigned long long wmax[WNW][WM];
-  const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
-  WfStage<WM> *st = reinterpret_cast<WfStage<WM> *>(smraw) + w * NSTG;
-  unsigned long long *bar =
-      reinterpret_cast<unsigned long long *>(smraw + (size_t)WNW * NSTG * sizeof(WfStage<WM>)) + w * NSTG;
+  const int l = threadIdx.x & 31;
+  WfStage<CR> *st = reinterpret_cast<WfStage<CR> *>(smraw);
+  unsigned long long *bar = reinterpret_cast<unsigned long long *>(smraw + (size_t)NSTG * sizeof(WfStage<CR>));
   unsigned long long tmax[WM][NS];
 #pragma unroll
   for (int i = 0; i < WM; ++i)
 #pragma unroll
     for (int s = 0; s < NS; ++s) tmax[i][s] = 0ull;
-  // (one warp per CTA: the item is blockIdx.x, provably warp-uniform, so the TMA
-  // coordinates below live in uniform registers)
-  const int item = WNW == 1 ? (int)blockIdx.x : (int)blockIdx.x * WNW + w;
-  if (item >= A.items && *(volatile int *)&A.ctl->k_done >= 0) return;  // (working warps: below)
-  if (item < A.items) {
-    const Geo &g = A.g;
-    // strip-major item order (consecutive CTAs = the segments of one strip): the
-    // warps streaming at the same time cover ~resident/segs strips over the whole
-    // height; measured 5-6 % faster than segment-row-major at 8192^2 (DRAM
-    // pattern).  IBM_WF_ORDER=0: segment-row-major; 1: scattered rows.
-    int sx = item / A.segs, sy = item % A.segs;
-    if (A.seg_mode == 1) {  // edge segments only (strip-major)
-      const int ne = A.e_lo + A.e_hi, k = item % ne;
-      sx = item / ne;
-      sy = k < A.e_lo ? k : A.segs - A.e_hi + (k - A.e_lo);
-    } else if (A.seg_mode == 2) {  // interior segments only
-      const int ni_ = A.segs - A.e_lo - A.e_hi;
-      sx = item / ni_;
-      sy = A.e_lo + item % ni_;
-    } else if (A.order == 0) {
-      sx = item % A.strips;
-      sy = item / A.strips;
-    } else if (A.order == 1) {
-      sx = item % A.strips;
-      sy = (int)(((long)(item / A.strips) * A.order_mul) % A.segs);
-    } else if (A.order == 3) {  // groups of order_g strips, segment-row-major inside a group
-      const int gsz = A.order_g * A.segs, g0 = (item / gsz) * A.order_g, r = item % gsz;
-      const int gw = min(A.order_g, A.strips - g0);
-      sx = g0 + r % gw;
-      sy = r / gw;
-    }
-    const int i0 = sx * OW - 2 * WM;  // global column of stored column 0
-    const int j0 = sy * A.L;          // owned local rows [j0, j1)
-    const int j1 = min(j0 + A.L, g.nj);
-    const int rs = j0 - 2 * WM;       // first streamed row
-    const int nch = ((j1 - j0) + 4 * WM + W - 1) / W;
-    if (l == 0) {
-      for (int s = 0; s < NSTG; ++s) mbar_init(&bar[s], 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncwarp();
-    for (int hc = 0; hc < NSTG - 1 && hc < 2 * nch; ++hc)  // halves 0..2; half hc+3 is issued in half hc
-      tma_load_pair_elect(&bar[hc], kBytes, &st[hc].x[0][0], &A.tmx, &st[hc].b[0][0], &A.tmb, i0,
-                          rs + hc * CR + kGhost);
-    // converged at an earlier iteration: nothing to do.  Tested after the first
-    // TMA issue so that the control-word round trip does not delay the item's
-    // first chunk; the loads in flight are waited for before leaving.
-    if (*(volatile int *)&A.ctl->k_done >= 0) {
-      for (int hc = 0; hc < NSTG - 1 && hc < 2 * nch; ++hc) mbar_wait_warp(&bar[hc], 0);
-      return;
-    }
+  const Geo &g = A.g;
+  const int stride = gridDim.x;
+  int item = blockIdx.x;  // (warp-uniform)
+  if (l == 0) {
+    for (int s = 0; s < NSTG; ++s) mbar_init(&bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  WfItem it = wf_item<WM, LAG>(A, item);
+  for (int hc = 0; hc < NSTG - 1 && hc < 2 * it.nch; ++hc)  // the first NSTG-1 halves
+    tma_load_pair_elect(&bar[hc], kBytes, &st[hc].x[0][0], &A.tmx, &st[hc].b[0][0], &A.tmb, it.i0,
+                        it.rs + hc * CR + kGhost);
+  // converged at an earlier iteration (host-batched passes): nothing to do.  Tested
+  // after the first TMA issue so that the control-word round trip does not delay
+  // the item's first chunk; the loads in flight are waited for before leaving.
+  if (*(volatile int *)&A.ctl->k_done >= 0) {
+    for (int hc = 0; hc < NSTG - 1 && hc < 2 * it.nch; ++hc) mbar_wait_warp(&bar[hc], 0);
+    return;
+  }
+  double2 X[NS][W], B[NS][W];
+#pragma unroll
+  for (int s = 0; s < NS; ++s)
+#pragma unroll
+    for (int q = 0; q < W; ++q) X[s][q] = B[s][q] = make_double2(0.0, 0.0);
+  int G = 0;  // ring index of the current item's half 0
+  for (; item < A.items; item += stride) {
+    const bool has_next = item + stride < A.items;
+    const WfItem nx = wf_item<WM, LAG>(A, has_next ? item + stride : item);
+    const int nh = 2 * it.nch, nhn = has_next ? 2 * nx.nch : 0;
+    const int i0 = it.i0, j0 = it.j0, j1 = it.j1, rs = it.rs, nch = it.nch;
     bool lane_own[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
@@ -419,9 +447,18 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
     }
     const bool interior = i0 >= A.ui0 && i0 + SC <= A.ui1;
     const bool boxstrip = !A.box.empty() && i0 < A.box.i1 && i0 + SC > A.box.i0;
-    // column coefficients (0 outside the family) and the reference row of the segment
-    const int jr = min(max(g.gj0 + j0 + A.L / 2, 1), g.NJ - 2);
-    const double cN0 = A.cN[jr], cS0 = A.cS[jr];
+    // the segment's reference row coefficients and its irregular streamed rows
+    // (outside the family or other row coefficients; host-built), plus the body box
+    const WfSeg sg = A.seg[it.sy];
+    const double cN0 = sg.cN0, cS0 = sg.cS0;
+    int irr0 = sg.irr0, irr1 = sg.irr1;
+    if (boxstrip) {
+      const int lo = max(A.box.j0, rs - DLO), hi = min(A.box.j1 - 1, rs + nch * W - 2);
+      if (lo <= hi) {
+        irr0 = min(irr0, lo);
+        irr1 = max(irr1, hi);
+      }
+    }
     WfCols C;
 #pragma unroll
     for (int s = 0; s < NS; ++s)
@@ -437,71 +474,50 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
         C.yu[s][e] = __drcp_rn((C.sEW[s][e] + (cN0 + cS0)) + C.cD[s][e]);
         C.inm[s][e] = (gi >= A.ui0 && gi < A.ui1) ? 0xffffffffu : 0u;
       }
-    double2 X[NS][W], B[NS][W];
-#pragma unroll
-    for (int s = 0; s < NS; ++s)
-#pragma unroll
-      for (int q = 0; q < W; ++q) X[s][q] = B[s][q] = make_double2(0.0, 0.0);
-    // Irregular rows of the item (outside the family, in the body box, or with
-    // row coefficients other than the reference): the chunks whose rows
-    // rb-2WM .. rb+W-2 meet [irr0, irr1] take the predicated path.
-    // (unconditional loads of clamped rows, unrolled: the loads of several rows
-    // are in flight together instead of one dependent L2 round trip per test)
-    int irr0 = INT_MAX, irr1 = INT_MIN;
-#pragma unroll 4
-    for (int r = rs - 2 * WM + l; r <= rs + nch * W - 2; r += 32) {
-      const int gj = g.gj0 + r;
-      const int gjc = min(max(gj, 0), g.NJ - 1);
-      const double cn = __ldg(A.cN + gjc), cs = __ldg(A.cS + gjc);
-      const bool reg = (gj >= A.uj0) & (gj < A.uj1) & !(boxstrip & (r >= A.box.j0) & (r < A.box.j1)) &
-                       (cn == cN0) & (cs == cS0);
-      if (!reg) {
-        irr0 = min(irr0, r);
-        irr1 = max(irr1, r);
-      }
-    }
-    irr0 = __reduce_min_sync(FULL, irr0);
-    irr1 = __reduce_max_sync(FULL, irr1);
     for (int c = 0; c < nch; ++c) {
       const int hA = 2 * c, hB = hA + 1;  // this window's halves
       const int rb = rs + c * W;
-      const bool fast = rb + W - 2 < irr0 || rb - 2 * WM > irr1;
-      const bool hasf = boxstrip && rb + W - 2 >= A.box.j0 && rb - 2 * WM < A.box.j1;
-      mbar_wait_warp(&bar[hA % NSTG], (hA / NSTG) & 1);
-      const bool ownall = rb - 2 * WM >= j0 && rb + W - 2 < j1;
-      // refill the stage of half h - 1 with half h + 3 once the first step of half h
-      // has read its last b row (see wf_nstg; for h = 0 that stage only supplied
-      // the b of the junk row rs - 1)
+      // (rows the chunk updates: rb - DLO .. rb + W - 2)
+      const bool fast = rb + W - 2 < irr0 || rb - DLO > irr1;
+      const bool hasf = boxstrip && rb + W - 2 >= A.box.j0 && rb - DLO < A.box.j1;
+      mbar_wait_warp(&bar[(G + hA) % NSTG], ((G + hA) / NSTG) & 1);
+      const bool ownall = rb - DLO >= j0 && rb + W - 2 < j1;
+      // refill the stage of half h - 1 with half h + 3 -- of this item, or of the
+      // next one near the end of this one -- once the first step of half h has read
+      // its last b row (see wf_nstg)
       auto refill = [&](int h) {
         __syncwarp();
-        const int hn = h + NSTG - 1;
-        if (hn < 2 * nch) {  // (warp-uniform)
-          const int sr = hn % NSTG;
-          tma_load_pair_elect(&bar[sr], kBytes, &st[sr].x[0][0], &A.tmx, &st[sr].b[0][0], &A.tmb, i0,
-                              rs + hn * CR + kGhost);
-        }
+        const int hn = h + NSTG - 1, sr = (G + hn) % NSTG;
+        const bool own_h = hn < nh;
+        const int hl = own_h ? hn : hn - nh;
+        const bool go = own_h || hl < nhn;  // (warp-uniform)
+        tma_load_pair_elect_if(go, &bar[sr], kBytes, &st[sr].x[0][0], &A.tmx, &st[sr].b[0][0], &A.tmb,
+                               own_h ? i0 : nx.i0, (own_h ? rs : nx.rs) + hl * CR + kGhost);
       };
       struct {
         decltype(refill) &rf;
         unsigned long long *bar;
-        int hA, hB;
-        __device__ void after_first() { rf(hA); }
-        __device__ void wait_second() { mbar_wait_warp(&bar[hB % NSTG], (hB / NSTG) & 1); }
-        __device__ void after_second() { rf(hB); }
-      } hooks{refill, bar, hA, hB};
-      const WfStage<WM> &SA = st[hA % NSTG], &SB = st[hB % NSTG], &Sp = st[(hA + NSTG - 1) % NSTG];
+        int gA, gB;
+        __device__ void after_first() { rf(gA); }
+        __device__ void wait_second() { mbar_wait_warp(&bar[(gB) % NSTG], ((gB) / NSTG) & 1); }
+        __device__ void after_second() { rf(gA + 1); }
+      } hooks{refill, bar, hA, G + hB};
+      const WfStage<CR> &SA = st[(G + hA) % NSTG], &SB = st[(G + hB) % NSTG],
+                        &Sp = st[(G + hA + NSTG - 1) % NSTG];
       if (fast && interior && ownall)
-        wf_chunk<WM, TP, 2, true, APX>(X, B, SA, SB, Sp, C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax, hooks);
+        wf_chunk<WM, LAG, TP, 2, true, APX>(X, B, SA, SB, Sp, C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax, hooks);
       else if (fast && interior)
-        wf_chunk<WM, TP, 2, false, APX>(X, B, SA, SB, Sp, C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax, hooks);
+        wf_chunk<WM, LAG, TP, 2, false, APX>(X, B, SA, SB, Sp, C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax, hooks);
       else if (fast)
-        wf_chunk<WM, TP, 1, false, APX>(X, B, SA, SB, Sp, C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax, hooks);
+        wf_chunk<WM, LAG, TP, 1, false, APX>(X, B, SA, SB, Sp, C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax, hooks);
       else
-        wf_chunk<WM, TP, 0, false, APX>(X, B, SA, SB, Sp, C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax, hooks);
+        wf_chunk<WM, LAG, TP, 0, false, APX>(X, B, SA, SB, Sp, C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax, hooks);
     }
+    G += nh;
+    it = nx;
   }
-  // residual of each fused iteration: warp -> CTA -> atomicMax on its bit pattern
-  // (halo pairs accumulated recomputed cells: dropped here)
+  // residual of each fused iteration over the CTA's items: lanes -> atomicMax on
+  // its bit pattern (halo pairs accumulated recomputed cells: dropped here)
 #pragma unroll
   for (int i = 0; i < WM; ++i) {
     unsigned long long t = 0ull;
@@ -512,383 +528,57 @@ __global__ void __launch_bounds__(WNT, wf_min_blocks<WM>()) k_sor_wf(const __gri
     }
 #pragma unroll
     for (int off = 16; off; off >>= 1) t = umax64(t, __shfl_xor_sync(FULL, t, off));
-    if (l == 0) wmax[w][i] = APX ? t << 32 : t;  // APX: the lower bound LB = H << 32
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int i = 0; i < WM; ++i) {
-      unsigned long long mx = 0;
-#pragma unroll
-      for (int v = 0; v < WNW; ++v) mx = umax64(mx, wmax[v][i]);
-      if (mx) atomicMax(&A.rho_bits[A.k + i], mx);
-    }
-    // The stop decision is taken by k_sor_check, launched after the pass (after the
-    // cross-slab reduction on decomposed grids): deciding in the pass's last CTA
-    // needs a __threadfence per CTA, which waits for the CTA's outstanding stores
-    // (ncu: ~5 % of the pass's stall samples at 8192^2).
+    // APX: the lower bound LB = H << 32.  The stop decision is k_sor_check's, after
+    // the pass (after the cross-slab reduction on decomposed grids): deciding in the
+    // pass's last CTA needs a __threadfence per CTA (ncu: ~5 % of the stall samples).
+    if (l == 0 && t) atomicMax(&A.rho_bits[A.k + i], APX ? t << 32 : t);
   }
 }
 
-// ============================================================================
-// Four contiguous columns per lane (CPL = 4): lane l holds the column pairs
-// (4l, 4l+1) and (4l+2, 4l+3) of a 128-column strip (128 - 4WM owned instead of
-// 64 - 4WM), so one half-sweep of a row needs one shuffle per two node updates
-// (the pair at the lane's other end reads its neighbour from the lane itself)
-// and the warp carries two independent updates per row and half-sweep.  The
-// register window is the same W = 2WM+2 rows; it arrives by TMA in two halves of
-// WM+1 rows (8 KB per half at WM = 3) so that three stages still fit eight warps
-// per SM.  Arithmetic, colours and the order of every update are those of the
-// CPL = 2 kernel above (and of the oracle): same FMA chain, same reciprocal.
-constexpr int SC4 = 128;  // stored columns per strip
-template <int WM>
-struct __align__(128) Wf4Stage {
-  double x[WM + 1][SC4];
-  double b[WM + 1][SC4];
-};
-template <int WM>
-constexpr size_t wf4_smem() {
-  return (size_t)(WPD + 1) * (sizeof(Wf4Stage<WM>) + sizeof(unsigned long long));
-}
-template <int WM>
-constexpr int wf4_min_blocks() {
-  return (int)((220u * 1024u) / wf4_smem<WM>()) < 8 ? (int)((220u * 1024u) / wf4_smem<WM>()) : 8;
-}
-
-struct Wf4Cols {  // [pair st][element e] of the lane's columns gi = i0 + 4l + 2st + e
-  double aE[2][2], aW[2][2], yu[2][2];
-  unsigned inm[2][2];
-};
-
-// the four (W, E) neighbours of the two pairs' element E in window slot Q
-template <int W, int Q, int E>
-__device__ __forceinline__ void wf4_nb(const double2 (&X)[W][2], double (&xw)[2], double (&xe)[2]) {
-  const int l = threadIdx.x & 31;
-  if (E == 0) {  // columns 4l, 4l+2: west of 4l is lane l-1's column 4l-1
-    xw[0] = __shfl_sync(FULL, X[Q][1].y, (l + 31) & 31);
-    xe[0] = X[Q][0].y;
-    xw[1] = X[Q][0].y;
-    xe[1] = X[Q][1].y;
-  } else {  // columns 4l+1, 4l+3: east of 4l+3 is lane l+1's column 4l+4
-    xw[0] = X[Q][0].x;
-    xe[0] = X[Q][1].x;
-    xw[1] = X[Q][1].x;
-    xe[1] = __shfl_sync(FULL, X[Q][0].x, (l + 1) & 31);
-  }
-}
-
-template <int W, int Q, int E, bool EDGE, bool APX>
-__device__ __forceinline__ void wf4_fast(double2 (&X)[W][2], const double2 (&B)[W][2], const Wf4Cols &C, double aN,
-                                         double aS, double omega, unsigned okm, unsigned long long (&tmax)[2]) {
-  constexpr int QN = (Q + 1) % W, QS = (Q + W - 1) % W;
-  double xw[2], xe[2];
-  wf4_nb<W, Q, E>(X, xw, xe);
-#pragma unroll
-  for (int st = 0; st < 2; ++st) {
-    const double xo = rd(X[Q][st], E), xN = rd(X[QN][st], E), xS = rd(X[QS][st], E);
-    const double nm = __fma_rn(aN, xN, __fma_rn(C.aE[st][E], xe[st], __fma_rn(C.aW[st][E], xw[st],
-                                                                               __fma_rn(aS, xS, rd(B[Q][st], E)))));
-    const double d = __fma_rn(nm, C.yu[st][E], -xo);  // gs - x_old, one rounding (R13)
-    const double xn = __fma_rn(omega, d, xo);
-    wr(X[Q][st], E, (!EDGE || C.inm[st][E]) ? xn : xo);
-    wf_acc<APX>(tmax[st], d, EDGE ? (okm & C.inm[st][E]) : okm);
-  }
-}
-
-template <int W, int Q, int E, bool APX>
-__device__ __forceinline__ void wf4_slow(double2 (&X)[W][2], const double2 (&B)[W][2], const Wf4Cols &C,
-                                         const WfArgs &A, int r, int i0, bool hasf, double omega, bool own,
-                                         unsigned long long (&tmax)[2]) {
-  constexpr int QN = (Q + 1) % W, QS = (Q + W - 1) % W;
-  const int l = threadIdx.x & 31;
-  const int gj = A.g.gj0 + r;
-  double cN = 0.0, cS = 0.0;  // 0 outside the family (oracle: out-of-range coefficient)
-  if (gj >= 0 && gj < A.g.NJ) {
-    cN = A.cN[gj];
-    cS = A.cS[gj];
-  }
-  double xw[2], xe[2];
-  wf4_nb<W, Q, E>(X, xw, xe);
-#pragma unroll
-  for (int st = 0; st < 2; ++st) {
-    const int gi = i0 + 4 * l + 2 * st + E;
-    const bool in = gi >= 0 && gi < A.g.ni;
-    bool u = gi >= A.ui0 && gi < A.ui1 && gj >= A.uj0 && gj < A.uj1;
-    uint8_t fl = 0;
-    // rows past the stored ghost rows are junk recomputation (never stored nor counted)
-    if (hasf && u && r >= -kGhost && r < A.g.nj + kGhost) fl = A.flag[A.g.off(gi, r)];
-    u = u && !(fl & PF_INACTIVE);
-    const double cD = in ? __ldg(A.cD + gi) : 0.0;
-    double aE = C.aE[st][E], aW = C.aW[st][E], aN = cN, aS = cS, aP;
-    if (fl) {
-      aE = (fl & PF_E) ? 0.0 : aE;
-      aW = (fl & PF_W) ? 0.0 : aW;
-      aN = (fl & PF_N) ? 0.0 : aN;
-      aS = (fl & PF_S) ? 0.0 : aS;
-      aP = ((aE + aW) + (aN + aS)) + cD;
-    } else {
-      aP = ((aE + aW) + (cN + cS)) + cD;
-    }
-    const double xo = rd(X[Q][st], E), xN = rd(X[QN][st], E), xS = rd(X[QS][st], E);
-    const double nm = __fma_rn(aN, xN, __fma_rn(aE, xe[st], __fma_rn(aW, xw[st], __fma_rn(aS, xS, rd(B[Q][st], E)))));
-    const double d = __fma_rn(nm, __drcp_rn(aP), -xo);
-    if (u) {
-      wr(X[Q][st], E, __fma_rn(omega, d, xo));
-      if (own) wf_acc<APX>(tmax[st], d, 0xffffffffu);
-    }
-  }
-}
-
-// One half (HALF = 0: slots 0..WM, 1: slots WM+1..2WM+1) of the window of W rows
-// rb .. rb+W-1; its rows come from stage S.
-template <int WM, int TP, int MODE, bool OWN, bool APX, int HALF>
-__device__ __forceinline__ void wf4_half(double2 (&X)[2 * WM + 2][2], double2 (&B)[2 * WM + 2][2],
-                                         const Wf4Stage<WM> &S, const Wf4Stage<WM> &Sp, const Wf4Cols &C,
-                                         const WfArgs &A, int rb, int j0,
-                                         int j1, int i0, const bool (&lane_own)[2], bool hasf, double cN0, double cS0,
-                                         unsigned long long (&tmax)[WM][2]) {
-  constexpr int W = 2 * WM + 2, CR = WM + 1;
-  const int l = threadIdx.x & 31;
-  const double omega = A.omega;
-  const long pitch = A.g.pitch;
-  double *const ob = A.xout + (long)(rb - 2 * WM + kGhost) * pitch + (i0 + 4 * l);
-  sfor<CR>([&](auto qc) {
-    constexpr int qq = decltype(qc)::value;
-    constexpr int q = HALF * CR + qq;  // window slot = row rb + q
-    // row rb+q enters the window; b of row rb+q-1 (first needed now) is read now,
-    // not with its x, which shortens its live range by one row (registers)
-    constexpr int qb = (q + W - 1) % W;
-#pragma unroll
-    for (int st = 0; st < 2; ++st) {
-      X[q][st] = *reinterpret_cast<const double2 *>(&S.x[qq][4 * l + 2 * st]);
-      B[qb][st] = *reinterpret_cast<const double2 *>(qq == 0 ? &Sp.b[CR - 1][4 * l + 2 * st]
-                                                              : &S.b[qq == 0 ? 0 : qq - 1][4 * l + 2 * st]);
-    }
-    sfor<2 * WM>([&](auto hc) {
-      constexpr int h = decltype(hc)::value;
-      constexpr int Q = ((q - 1 - h) % W + W) % W;  // slot of row rb + q - 1 - h
-      constexpr int E = (TP + Q + h) & 1;           // red (h even): (i + j) even
-      const int r = rb + q - 1 - h;
-      [[maybe_unused]] const bool own = OWN || (r >= j0 && r < j1);
-      unsigned okm = 0xffffffffu;
-      if (!OWN)
-        asm("{\n .reg .b32 t;\n or.b32 t, %1, %2;\n shr.s32 t, t, 31;\n not.b32 %0, t;\n}"
-            : "=r"(okm)
-            : "r"(r - j0), "r"(j1 - 1 - r));
-      if constexpr (MODE > 0)
-        wf4_fast<W, Q, E, MODE == 1, APX>(X, B, C, cN0, cS0, omega, okm, tmax[h / 2]);
-      else
-        wf4_slow<W, Q, E, APX>(X, B, C, A, r, i0, hasf, omega, own, tmax[h / 2]);
-    });
-    const int ro = rb + q - 2 * WM;  // row that has received its last half-sweep
-    const bool rowin = OWN || (ro >= j0 && ro < j1);
-#pragma unroll
-    for (int st = 0; st < 2; ++st) {
-      const double2 v = X[((q - 2 * WM) % W + W) % W][st];
-      const bool pair_in = MODE == 2 || i0 + 4 * l + 2 * st + 1 < A.g.ni;
-      st_pred(rowin && lane_own[st] && pair_in, ob + q * pitch + 2 * st, v);
-      if (MODE < 2) st_pred1(rowin && lane_own[st] && !pair_in, ob + q * pitch + 2 * st, v.x);
-    }
-  });
-}
-
-template <int WM, int TP, int MODE, bool OWN, bool APX>
-__device__ __forceinline__ void wf4_window(double2 (&X)[2 * WM + 2][2], double2 (&B)[2 * WM + 2][2],
-                                           Wf4Stage<WM> *st, unsigned long long *bar, const Wf4Cols &C,
-                                           const WfArgs &A, int c, int nhc, int rs, int rb, int j0, int j1, int i0,
-                                           const bool (&lane_own)[2], bool hasf, double cN0, double cS0,
-                                           unsigned long long (&tmax)[WM][2]) {
-  constexpr int NSTG = WPD + 1, CR = WM + 1;
-  constexpr unsigned kHalf = 2u * CR * SC4 * 8;
-  const int l = threadIdx.x & 31;
-  auto refill = [&](int hc) {
-    __syncwarp();
-    if (l == 0 && hc + WPD < nhc) {
-      // stage of half-window hc - 1: every lane consumed its values before the __syncwarp
-      const int h2 = hc + WPD, sr = h2 % NSTG;
-      mbar_expect_tx(&bar[sr], kHalf);
-      tma_load_2d(&st[sr].x[0][0], &A.tmx, i0, rs + h2 * CR + kGhost, &bar[sr]);
-      tma_load_2d(&st[sr].b[0][0], &A.tmb, i0, rs + h2 * CR + kGhost, &bar[sr]);
-    }
-  };
-  // (the first window's "previous" stage is its own: the b it supplies there
-  // belongs to row rs-1, a junk row never stored nor counted)
-  const int h0 = 2 * c, h1 = 2 * c + 1, hp = c > 0 ? h0 - 1 : h0;
-  mbar_wait_warp(&bar[h0 % NSTG], (h0 / NSTG) & 1);
-  wf4_half<WM, TP, MODE, OWN, APX, 0>(X, B, st[h0 % NSTG], st[hp % NSTG], C, A, rb, j0, j1, i0, lane_own, hasf, cN0,
-                                      cS0, tmax);
-  refill(h0);
-  mbar_wait_warp(&bar[h1 % NSTG], (h1 / NSTG) & 1);
-  wf4_half<WM, TP, MODE, OWN, APX, 1>(X, B, st[h1 % NSTG], st[h0 % NSTG], C, A, rb, j0, j1, i0, lane_own, hasf, cN0,
-                                      cS0, tmax);
-  refill(h1);
-}
-
-template <int WM, int TP, bool APX>
-__global__ void __launch_bounds__(32, wf4_min_blocks<WM>()) k_sor_wf4(const __grid_constant__ WfArgs A) {
-  constexpr int W = 2 * WM + 2, OW = SC4 - 4 * WM, NSTG = WPD + 1, CR = WM + 1;
-  constexpr unsigned kHalf = 2u * CR * SC4 * 8;
-  extern __shared__ __align__(1024) unsigned char smraw[];
-  const int l = threadIdx.x & 31;
-  Wf4Stage<WM> *st = reinterpret_cast<Wf4Stage<WM> *>(smraw);
-  unsigned long long *bar = reinterpret_cast<unsigned long long *>(smraw + (size_t)NSTG * sizeof(Wf4Stage<WM>));
-  unsigned long long tmax[WM][2];
-#pragma unroll
-  for (int i = 0; i < WM; ++i) tmax[i][0] = tmax[i][1] = 0ull;
-  const int item = blockIdx.x;
-  const Geo &g = A.g;
-  int sx = item / A.segs, sy = item % A.segs;  // strip-major item order
-  if (A.seg_mode == 1) {  // edge / interior subsets (decomposed grids), as in k_sor_wf
-    const int ne = A.e_lo + A.e_hi, k = item % ne;
-    sx = item / ne;
-    sy = k < A.e_lo ? k : A.segs - A.e_hi + (k - A.e_lo);
-  } else if (A.seg_mode == 2) {
-    const int ni_ = A.segs - A.e_lo - A.e_hi;
-    sx = item / ni_;
-    sy = A.e_lo + item % ni_;
-  } else if (A.order == 0) {
-    sx = item % A.strips;
-    sy = item / A.strips;
-  }
-  const int i0 = sx * OW - 2 * WM;  // global column of stored column 0
-  const int j0 = sy * A.L;          // owned local rows [j0, j1)
-  const int j1 = min(j0 + A.L, g.nj);
-  const int rs = j0 - 2 * WM;       // first streamed row
-  const int nwin = ((j1 - j0) + 4 * WM + W - 1) / W;
-  const int nhc = 2 * nwin;
-  if (l == 0) {
-    for (int s = 0; s < NSTG; ++s) mbar_init(&bar[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int h = 0; h < WPD && h < nhc; ++h) {
-      mbar_expect_tx(&bar[h], kHalf);
-      tma_load_2d(&st[h].x[0][0], &A.tmx, i0, rs + h * CR + kGhost, &bar[h]);
-      tma_load_2d(&st[h].b[0][0], &A.tmb, i0, rs + h * CR + kGhost, &bar[h]);
-    }
-  }
-  __syncwarp();
-  if (*(volatile int *)&A.ctl->k_done >= 0) {  // converged at an earlier iteration
-    for (int h = 0; h < WPD && h < nhc; ++h) mbar_wait_warp(&bar[h], 0);
-    return;
-  }
-  bool lane_own[2];
-#pragma unroll
-  for (int s = 0; s < 2; ++s) {
-    const int p = 2 * l + s;  // pair index in the strip
-    lane_own[s] = p >= WM && p <= SC4 / 2 - 1 - WM && i0 + 2 * p < g.ni;
-  }
-  const bool interior = i0 >= A.ui0 && i0 + SC4 <= A.ui1;
-  const bool boxstrip = !A.box.empty() && i0 < A.box.i1 && i0 + SC4 > A.box.i0;
-  const int jr = min(max(g.gj0 + j0 + A.L / 2, 1), g.NJ - 2);
-  const double cN0 = A.cN[jr], cS0 = A.cS[jr];
-  Wf4Cols C;
-#pragma unroll
-  for (int s = 0; s < 2; ++s)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int gi = i0 + 4 * l + 2 * s + e;
-      const bool in = gi >= 0 && gi < g.ni;
-      const double cE = in ? A.cE[gi] : 0.0, cW = in ? A.cW[gi] : 0.0, cD = in ? A.cD[gi] : 0.0;
-      C.aE[s][e] = cE;
-      C.aW[s][e] = cW;
-      C.yu[s][e] = __drcp_rn(((cE + cW) + (cN0 + cS0)) + cD);
-      C.inm[s][e] = (gi >= A.ui0 && gi < A.ui1) ? 0xffffffffu : 0u;
-    }
-  double2 X[W][2], B[W][2];
-#pragma unroll
-  for (int q = 0; q < W; ++q) X[q][0] = X[q][1] = B[q][0] = B[q][1] = make_double2(0.0, 0.0);
-  int irr0 = INT_MAX, irr1 = INT_MIN;
-#pragma unroll 4
-  for (int r = rs - 2 * WM + l; r <= rs + nwin * W - 2; r += 32) {
-    const int gj = g.gj0 + r;
-    const int gjc = min(max(gj, 0), g.NJ - 1);
-    const double cn = __ldg(A.cN + gjc), cs = __ldg(A.cS + gjc);
-    const bool reg = (gj >= A.uj0) & (gj < A.uj1) & !(boxstrip & (r >= A.box.j0) & (r < A.box.j1)) &
-                     (cn == cN0) & (cs == cS0);
-    if (!reg) {
-      irr0 = min(irr0, r);
-      irr1 = max(irr1, r);
-    }
-  }
-  irr0 = __reduce_min_sync(FULL, irr0);
-  irr1 = __reduce_max_sync(FULL, irr1);
-  for (int c = 0; c < nwin; ++c) {
-    const int rb = rs + c * W;
-    const bool fast = rb + W - 2 < irr0 || rb - 2 * WM > irr1;
-    const bool hasf = boxstrip && rb + W - 2 >= A.box.j0 && rb - 2 * WM < A.box.j1;
-    const bool ownall = rb - 2 * WM >= j0 && rb + W - 2 < j1;
-    if (fast && interior && ownall)
-      wf4_window<WM, TP, 2, true, APX>(X, B, st, bar, C, A, c, nhc, rs, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax);
-    else if (fast && interior)
-      wf4_window<WM, TP, 2, false, APX>(X, B, st, bar, C, A, c, nhc, rs, rb, j0, j1, i0, lane_own, hasf, cN0, cS0,
-                                        tmax);
-    else if (fast)
-      wf4_window<WM, TP, 1, false, APX>(X, B, st, bar, C, A, c, nhc, rs, rb, j0, j1, i0, lane_own, hasf, cN0, cS0,
-                                        tmax);
-    else
-      wf4_window<WM, TP, 0, false, APX>(X, B, st, bar, C, A, c, nhc, rs, rb, j0, j1, i0, lane_own, hasf, cN0, cS0,
-                                        tmax);
-  }
-  // residual of each fused iteration: lanes -> warp -> atomicMax on the bit pattern
-  // (halo pairs accumulated recomputed cells: dropped here); the stop decision is
-  // k_sor_check's, after the pass
-#pragma unroll
-  for (int i = 0; i < WM; ++i) {
-    unsigned long long t = 0ull;
-#pragma unroll
-    for (int s = 0; s < 2; ++s)
-      if (2 * l + s >= WM && 2 * l + s <= SC4 / 2 - 1 - WM) t = umax64(t, wf_res_word<APX>(tmax[i][s]));
-#pragma unroll
-    for (int off = 16; off; off >>= 1) t = umax64(t, __shfl_xor_sync(FULL, t, off));
-    if (l == 0 && t) atomicMax(&A.rho_bits[A.k + i], APX ? t << 32 : t);  // APX: LB = H << 32
-  }
-}
-
-template <int WM, int TP, bool APX>
-void wf4_prepare() {
-  static bool done = false;
-  if (!done) {
-    cudaFuncSetAttribute(k_sor_wf4<WM, TP, APX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wf4_smem<WM>());
-    done = true;
-  }
-}
-
-template <int WM, bool APX>
-void wf4_launch_tp(const WfArgs &a, cudaStream_t s) {
-  if (a.g.gj0 & 1) {
-    wf4_prepare<WM, 1, APX>();
-    k_sor_wf4<WM, 1, APX><<<a.items, 32, wf4_smem<WM>(), s>>>(a);
-  } else {
-    wf4_prepare<WM, 0, APX>();
-    k_sor_wf4<WM, 0, APX><<<a.items, 32, wf4_smem<WM>(), s>>>(a);
-  }
-}
-
-template <int WM, int TP, bool APX>
+template <int WM, int LAG, int TP, bool APX>
 int wf_blocks_per_sm() {
   static int per = 0;
   if (!per) {
-    cudaFuncSetAttribute(k_sor_wf<WM, TP, APX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wf_smem<WM>());
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sor_wf<WM, TP, APX>, WNT, wf_smem<WM>());
+    cudaFuncSetAttribute(k_sor_wf<WM, LAG, TP, APX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)wf_smem<WM, LAG>());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sor_wf<WM, LAG, TP, APX>, WNT, wf_smem<WM, LAG>());
     if (per < 1) per = 1;
   }
   return per;
 }
 
-template <int WM, bool APX>
+int sm_count();
+// One CTA per item (default): the hardware hands a freed slot the next item in
+// order, so the items streaming at the same time stay a compact range (DRAM
+// pattern, L2 reuse of the overlapping strip columns).  IBM_WF_PERSIST=1: one CTA
+// per resident slot taking every gridDim-th item, with the next item's first
+// halves prefetched across the item boundary -- measured slower (8192^2: 0.156
+// ms per iteration at the best L against 0.111): the static assignment lets the
+// concurrently streamed items drift apart (27.9 % L2 hits against 32.8 %, and
+// 24 % of the stall samples waiting for TMA data against 6 %).
+static bool wf_persist() {
+  static const bool p = [] {
+    const char *e = std::getenv("IBM_WF_PERSIST");
+    return e && std::atoi(e) == 1;
+  }();
+  return p;
+}
+template <int WM, int LAG, bool APX>
 void wf_launch_tp(const WfArgs &a, cudaStream_t s) {
-  const int grid = (a.items + WNW - 1) / WNW;
   if (a.g.gj0 & 1) {
-    wf_blocks_per_sm<WM, 1, APX>();
-    k_sor_wf<WM, 1, APX><<<grid, WNT, wf_smem<WM>(), s>>>(a);
+    const int grid = wf_persist() ? std::min(a.items, wf_blocks_per_sm<WM, LAG, 1, APX>() * sm_count()) : a.items;
+    wf_blocks_per_sm<WM, LAG, 1, APX>();
+    k_sor_wf<WM, LAG, 1, APX><<<grid, WNT, wf_smem<WM, LAG>(), s>>>(a);
   } else {
-    wf_blocks_per_sm<WM, 0, APX>();
-    k_sor_wf<WM, 0, APX><<<grid, WNT, wf_smem<WM>(), s>>>(a);
+    const int grid = wf_persist() ? std::min(a.items, wf_blocks_per_sm<WM, LAG, 0, APX>() * sm_count()) : a.items;
+    wf_blocks_per_sm<WM, LAG, 0, APX>();
+    k_sor_wf<WM, LAG, 0, APX><<<grid, WNT, wf_smem<WM, LAG>(), s>>>(a);
   }
 }
 
-// approximate residual on every solve: single slab (decision by the pass's last
-// CTA) and decomposed (max over ranks of the bounds, k_sor_check with apx = 1);
-// the exact instantiation (APX = false) is kept for experiments (WF_EXACT)
+// approximate residual on every solve: single slab and decomposed (max over ranks
+// of the bounds, k_sor_check with apx = 1); the exact instantiation (APX = false)
+// is kept for experiments (WF_EXACT)
 template <int WM>
 cudaError_t wf_launch(const WfArgs &a, cudaStream_t s) {
 #ifdef WF_EXACT
@@ -896,32 +586,34 @@ cudaError_t wf_launch(const WfArgs &a, cudaStream_t s) {
 #else
   constexpr bool kApx = true;
 #endif
-  if (wf_cpl() == 4)
-    wf4_launch_tp<WM, kApx>(a, s);
+  if (wf_lag() == 2)
+    wf_launch_tp<WM, 2, kApx>(a, s);
   else
-    wf_launch_tp<WM, kApx>(a, s);
+    wf_launch_tp<WM, 1, kApx>(a, s);
   return cudaGetLastError();
 }
 
 }  // namespace
 
-// columns per lane of the fused pass (2: 64-column strips, 4: 128-column strips),
-// fixed per process (the TMA boxes are built at init); IBM_WF_CPL overrides
-int wf_cpl() {
-  static const int cpl = [] {
-    const char *e = std::getenv("IBM_WF_CPL");
-    const int v = e ? std::atoi(e) : WF_CPL_DEFAULT;
-    return v == 4 ? 4 : 2;
+// half-sweep lag of the fused pass (1 or 2), fixed per process (the TMA box height
+// is built at init); IBM_WF_LAG overrides
+int wf_lag() {
+  static const int lag = [] {
+    const char *e = std::getenv("IBM_WF_LAG");
+    const int v = e ? std::atoi(e) : WF_LAG_DEFAULT;
+    return v == 2 ? 2 : 1;
   }();
-  return cpl;
+  return lag;
 }
-int wf_box_rows(int m) { return m + 1; }  // half a window (both layouts)
+static int wf_dlo(int m) { return 1 + wf_lag() * (2 * m - 1); }
+static int wf_w(int m) { return (wf_dlo(m) + 3) & ~1; }
+int wf_box_rows(int m) { return wf_w(m) / 2; }  // half a window
 #ifdef WF_EXACT
 bool wf_approx() { return false; }
 #else
 bool wf_approx() { return true; }
 #endif
-int wf_box_cols() { return wf_cpl() == 4 ? SC4 : SC; }
+int wf_box_cols() { return SC; }
 
 // Strip / segment plan: segments of L owned rows, L = 64 for m = 2 and 256 for
 // m >= 3, halved (down to 32 / 64) while the items would not fill two waves
@@ -934,7 +626,7 @@ int wf_box_cols() { return wf_cpl() == 4 ? SC4 : SC; }
 // to even so colours stay compile-time.
 namespace {
 // SM count of the current device (cached per device ordinal)
-int sm_count() {
+int sm_count_impl() {
   static int cache[64] = {0};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -946,7 +638,7 @@ int sm_count() {
   return sms;
 }
 // two waves of the 8 resident warps per SM
-int wf_items_target() { return 2 * 8 * sm_count(); }
+int wf_items_target() { return 2 * 8 * sm_count_impl(); }
 int wf_rows_default(int m) { return m == 2 ? 64 : 256; }
 int wf_rows_min(int m) { return m == 2 ? 32 : 64; }
 int wf_strips(int ni, int m) {
@@ -1021,6 +713,35 @@ void wf_plan(WfArgs &a, int m, int L_force) {
     while (y) { const int t = x % y; x = y; y = t; }
     if (x == 1) { a.order_mul = mlt; break; }
   }
+}
+
+namespace {
+int sm_count() { return sm_count_impl(); }
+}  // namespace
+
+std::vector<WfSeg> wf_seg_table(const WfArgs &a, int m, const double *cN, const double *cS) {
+  const int W = wf_w(m), DLO = wf_dlo(m), NJ = a.g.NJ;
+  std::vector<WfSeg> t(a.segs);
+  for (int sy = 0; sy < a.segs; ++sy) {
+    const int j0 = sy * a.L, j1 = std::min(j0 + a.L, a.g.nj), rs = j0 - 2 * m;
+    const int nch = ((j1 - j0) + 2 * m + DLO + W - 1) / W;
+    // the segment's reference row (as the kernel used to pick it)
+    const int jr = std::min(std::max(a.g.gj0 + j0 + a.L / 2, 1), NJ - 2);
+    WfSeg &e = t[sy];
+    e.cN0 = cN[jr];
+    e.cS0 = cS[jr];
+    e.irr0 = INT_MAX;
+    e.irr1 = INT_MIN;
+    for (int r = rs - DLO; r <= rs + nch * W - 2; ++r) {  // the rows the item updates
+      const int gj = a.g.gj0 + r, gjc = std::min(std::max(gj, 0), NJ - 1);
+      const bool reg = gj >= a.uj0 && gj < a.uj1 && cN[gjc] == e.cN0 && cS[gjc] == e.cS0;
+      if (!reg) {
+        e.irr0 = std::min(e.irr0, r);
+        e.irr1 = std::max(e.irr1, r);
+      }
+    }
+  }
+  return t;
 }
 
 cudaError_t launch_sor_wf(const WfArgs &a, int m, cudaStream_t s) {
