@@ -171,8 +171,13 @@ IBM_API int ibm_poisson_iterate(ibm_ctx *ctx, int iters, double *rho_out);
  *   IBM_QUERY_SLABS slabs held by this ctx (loopback: nranks, else 1)
  *   IBM_QUERY_TB_M  Poisson iterations per grid barrier of the resident persistent
  *                   solve used on mid-size single-slab grids (0 = not used)
+ *   IBM_QUERY_PEER_HALO 1 if the decomposed fused Poisson pass stores its boundary
+ *                   rows directly into the neighbouring slabs' ghost rows (loopback
+ *                   slabs, or ranks whose neighbours' buffers were mapped by CUDA IPC;
+ *                   SURVEY 8(f) f3; IBM_PEER_HALO=0 disables), 0 if the rows go
+ *                   through NCCL send/recv
  * IBM_ERR_ARG for an unknown key or NULL pointers.  No device work. */
-enum { IBM_QUERY_WF_M = 0, IBM_QUERY_WF_L = 1, IBM_QUERY_SLABS = 2, IBM_QUERY_TB_M = 3 };
+enum { IBM_QUERY_WF_M = 0, IBM_QUERY_WF_L = 1, IBM_QUERY_SLABS = 2, IBM_QUERY_TB_M = 3, IBM_QUERY_PEER_HALO = 4 };
 IBM_API int ibm_query(const ibm_ctx *ctx, int key, int *out);
 
 /* Human-readable cause of the last error on ctx (never NULL). */

@@ -295,7 +295,7 @@ bool make_coef_maps(Ctx &c) {
   const int ncol[3] = {c.nx + 1, c.nx, c.nx}, nrow[3] = {c.ny, c.ny + 1, c.ny};
   for (int f = 0; f < 3; ++f)
     for (int k = 0; k < 5; ++k)
-      if (!make_map_1d(&c.tm_coef[f][k], arr[f][k], k < 3 ? ncol[f] : nrow[f], k < 3 ? kSorBoxW : kSorBoxHx)) {
+      if (!make_map_1d(&c.tm_coef[f][k], arr[f][k], k < 3 ? ncol[f] : nrow[f], k < 3 ? kSorBoxW : kSorBoxRows1d)) {
         c.err = "cuTensorMapEncodeTiled (coefficients f=" + std::to_string(f) + " k=" + std::to_string(k) +
                 " n=" + std::to_string(k < 3 ? ncol[f] : nrow[f]) + " ptr%256=" +
                 std::to_string((uintptr_t)arr[f][k] % 256) + " map%64=" + std::to_string((uintptr_t)&c.tm_coef[f][k] % 64) +
@@ -429,6 +429,26 @@ int refresh_time(Ctx &c) {
 // CTA takes the convergence decision on the device; if it stops at an iteration
 // inside a fused pass, that pass is replayed from its (intact) input buffer up to
 // the decided iteration.  *buf_out receives the buffer index of the result.
+// IBM_DEBUG_SYNC=1: synchronise and check after every phase of a step (locates a
+// faulting kernel; debugging only)
+static bool debug_sync() {
+  static const bool on = [] {
+    const char *e = std::getenv("IBM_DEBUG_SYNC");
+    return e && std::atoi(e) == 1;
+  }();
+  return on;
+}
+#define DSYNC(tag)                                                                    \
+  do {                                                                                \
+    if (debug_sync()) {                                                               \
+      cudaError_t e_ = cudaStreamSynchronize(c.stream);                               \
+      if (e_ != cudaSuccess) {                                                        \
+        c.err = std::string("after ") + (tag) + ": " + cudaGetErrorString(e_);        \
+        return IBM_ERR_CUDA;                                                          \
+      }                                                                               \
+    }                                                                                 \
+  } while (0)
+
 // The fused pass's per-segment table (WfSeg) for slab r at the plan's segment
 // length: built on the host from the row coefficients once per (slab, L) and
 // uploaded on the solver stream; kept until ibm_destroy.
@@ -578,6 +598,7 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
   // decomposed fused passes: an exchange of the last pass's output may be in
   // flight on the comm stream; the main stream joins it before touching ghost rows
   bool halo_ready = false;
+  bool peer_ready = false;  // ghost rows of buffer `cur` hold the neighbours' rows (peer-halo passes)
   auto join_comm = [&]() -> int {
     if (halo_ready) CK(cudaStreamWaitEvent(c.stream, c.ev_halo, 0));
     halo_ready = false;
@@ -586,6 +607,7 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
   // one single-iteration pass of every slab (halos first when decomposed)
   auto single = [&](int kk, int in, bool fixup) -> int {
     const int out = in ^ 1;
+    peer_ready = false;  // (its output's ghost rows are not written)
     if (mult) {
       if (int e = join_comm()) return e;
       if (helm) {
@@ -606,8 +628,10 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
       } else {
         a.f[0].xin = s.phi[in]; a.f[0].xout = s.phi[out]; a.f[0].tmx = s.tm_phi[in]; a.f[0].tmb = s.tm_bp;
       }
+      DSYNC("sor halo / previous pass");
       launch_sor_iteration(a, c.stream, grids[r]);
       ++c.launches;
+      DSYNC(helm ? "k_sor<1> iteration" : "k_sor<0> iteration");
     }
     if (mult && !fixup) {
       if (!c.loopback)
@@ -647,7 +671,43 @@ int sor_solve(Ctx &c, bool helm, int s0, int *k_out, double *rho_out, int *statu
   for (;;) {
     const int kend = std::min(maxit, k + batch - 1);
     while (k <= kend) {
-      if (wf && mult && k + c.wf_m - 1 <= maxit) {
+      if (wf && mult && c.peer_halo && k + c.wf_m - 1 <= maxit) {
+        // Decomposed grid, device-initiated halo (f3): each slab's pass also stores its
+        // 2m boundary rows of output straight into the neighbours' ghost rows of their
+        // next input buffer (loopback: the other slabs' buffers; ranks: CUDA-IPC
+        // mappings over NVLink).  The per-pass residual all-reduce orders those
+        // stores before any rank's next pass (each rank contributes only after its
+        // pass kernel completed), so no further exchange or flag is needed.  The
+        // first pass of a solve, and the first after one-iteration passes, exchanges
+        // its input's ghost rows once.
+        const int in = cur;
+        if (!peer_ready) HALO_ROWS(2 * c.wf_m, (*b = s.phi[in], *g = &s.gp));
+        for (size_t r = 0; r < c.sl.size(); ++r) {
+          WfArgs wa = was[r];
+          wa.k = k;
+          wa.xout = c.sl[r].phi[in ^ 1];
+          wa.tmx = c.sl[r].tm_wphi[in];
+          wa.peer_rows = 2 * c.wf_m;
+          const long pitch = c.sl[r].gp.pitch;
+          if (c.loopback) {
+            wa.peer_lo = r > 0 ? c.sl[r - 1].phi[in ^ 1] + (long)c.sl[r - 1].gp.nj * pitch : nullptr;
+            wa.peer_hi = r + 1 < c.sl.size() ? c.sl[r + 1].phi[in ^ 1] - (long)c.sl[r].gp.nj * pitch : nullptr;
+          } else {
+            wa.peer_lo = c.peer_phi[0][in ^ 1] ? c.peer_phi[0][in ^ 1] + (long)c.peer_nj[0] * pitch : nullptr;
+            wa.peer_hi = c.peer_phi[1][in ^ 1] ? c.peer_phi[1][in ^ 1] - (long)c.sl[r].gp.nj * pitch : nullptr;
+          }
+          CK(launch_sor_wf(wa, c.wf_m, c.stream));
+          ++c.launches;
+        }
+        if (!c.loopback)
+          NK(ncclAllReduce(c.rho_bits + k, c.rho_bits + k, c.wf_m, ncclUint64, ncclMax, (ncclComm_t)c.nccl,
+                           c.stream));
+        launch_sor_check(c.ctl, c.rho_bits, k, maxit, cfg.check_every, tol, c.stream, c.wf_m, wf_approx() ? 1 : 0);
+        ++c.launches;
+        passes.push_back({k, c.wf_m, cur});
+        k += c.wf_m;
+        peer_ready = true;
+      } else if (wf && mult && k + c.wf_m - 1 <= maxit) {
         // Decomposed grid: the 2m halo rows of this pass's input arrived on the comm
         // stream (the first pass: exchanged here); the edge segments (those that read
         // ghost rows) run first, then the interior ones while the comm stream already
@@ -811,7 +871,9 @@ int step_once(Ctx &c, ibm_step_stats *st) {
   if (c.body.has)
     for (Slab &s : c.sl) {
       c.launches += launch_classify(c, s, yb);
+      DSYNC("classify");
       c.launches += launch_pflags(c, s);
+      DSYNC("pflags");
     }
   CK(cudaEventRecord(c.ev[7], c.stream));
   // N1 halos of u^n, v^n, p^n, then a2/a3 predictor
@@ -820,8 +882,10 @@ int step_once(Ctx &c, ibm_step_stats *st) {
     HALO((*b = s.v, *g = &s.gv));
     HALO((*b = s.p, *g = &s.gp));
   }
+  DSYNC("halo u v p");
   for (Slab &s : c.sl) c.launches += launch_predictor(c, s, yb, vb);
   CK(cudaGetLastError());
+  DSYNC("predictor");
   // the fused red-black pass also updates red on the first ghost row: it needs
   // the neighbour's right-hand side there
   if (multi(c)) {
@@ -829,6 +893,7 @@ int step_once(Ctx &c, ibm_step_stats *st) {
     HALO((*b = s.rv, *g = &s.gv));
   }
   CK(cudaEventRecord(c.ev[1], c.stream));
+  DSYNC("halo rhs");
   // a4 velocity (Helmholtz) SOR, u and v jointly (R5)
   int ku = 0, sst = 0;
   double rho_uv = 0.0;
@@ -836,6 +901,7 @@ int step_once(Ctx &c, ibm_step_stats *st) {
   int r = sor_solve(c, true, 0, &ku, &rho_uv, &sst, 0, &ures);
   if (r) return r;
   if (st) { st->it_uv = ku; st->rho_uv = rho_uv; }
+  DSYNC("velocity SOR");
   if (sst == 3) { c.err = "velocity SOR residual is NaN at step " + std::to_string(c.step + 1); return IBM_ERR_DIVERGED; }
   if (sst == 1) status = IBM_WARN_NOCONV;
   // the outlet fill (R10b) reads v* one row up: exchange v* first, then u*
@@ -843,10 +909,12 @@ int step_once(Ctx &c, ibm_step_stats *st) {
   for (Slab &s : c.sl) c.launches += launch_outlet_fill(c, s, s.us[ures], s.vs[ures]);
   if (multi(c)) HALO((*b = s.us[ures], *g = &s.gu));
   CK(cudaEventRecord(c.ev[2], c.stream));
+  DSYNC("outlet fill + halos");
   // a5 masks -> q, Poisson rhs; phi := 0 on inactive cells
   for (Slab &s : c.sl) c.launches += launch_prhs(c, s, s.us[ures], s.vs[ures], s.phi[c.phi_cur]);
   if (multi(c)) HALO_ROWS(c.wf_m >= 2 ? 2 * c.wf_m : 2, (*b = s.bp, *g = &s.gp));
   CK(cudaEventRecord(c.ev[3], c.stream));
+  DSYNC("poisson rhs");
   // a6 Poisson SOR, warm start
   int kp = 0;
   double rho_p = 0.0;
@@ -854,6 +922,7 @@ int step_once(Ctx &c, ibm_step_stats *st) {
   r = sor_solve(c, false, c.phi_cur, &kp, &rho_p, &sst, 0, &pbuf);
   if (r) return r;
   if (st) { st->it_p = kp; st->rho_p = rho_p; }
+  DSYNC("poisson SOR");
   if (sst == 3) { c.err = "pressure SOR residual is NaN at step " + std::to_string(c.step + 1); return IBM_ERR_DIVERGED; }
   if (sst == 1) status = IBM_WARN_NOCONV;
   c.phi_cur = pbuf;
@@ -865,6 +934,7 @@ int step_once(Ctx &c, ibm_step_stats *st) {
   if (c.body.has)
     for (Slab &s : c.sl) c.launches += launch_pext(c, s, s.phi[c.phi_cur]);
   CK(cudaEventRecord(c.ev[5], c.stream));
+  DSYNC("correct");
   // history rotation
   for (Slab &s : c.sl) {
     std::swap(s.cu, s.cup);
@@ -939,6 +1009,81 @@ int ibm_nccl_unique_id(unsigned char out[128]) {
   return IBM_OK;
 }
 
+// Device-initiated halo across ranks (f3): every rank publishes a CUDA-IPC handle
+// of the allocation holding its phi buffers (the caller's workspace) with their
+// offsets and owned rows (NCCL all-gather); each rank maps its two neighbours'
+// allocations.  All ranks then agree (all-reduce min) on whether every mapping
+// succeeded: the peer-store passes and the NCCL-exchange passes issue different
+// collectives, so either all ranks use them or none does.  Failure to map is not
+// an error (the NCCL halo path stays in use); a failed collective is.
+typedef CUresult (*PFN_memGetAddressRange)(CUdeviceptr *, size_t *, CUdeviceptr);
+static int open_peer_halo(Ctx &c) {
+  struct PeerInfo {
+    cudaIpcMemHandle_t h;
+    long long off[2];
+    int nj, ok;
+  };
+  PeerInfo mine;
+  std::memset(&mine, 0, sizeof(mine));
+  static PFN_memGetAddressRange range_fn = nullptr;
+  if (!range_fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      range_fn = reinterpret_cast<PFN_memGetAddressRange>(p);
+  }
+  const Slab &s0 = c.sl[0];
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range_fn && range_fn(&base, &size, (CUdeviceptr)s0.phi[0]) == CUDA_SUCCESS &&
+      cudaIpcGetMemHandle(&mine.h, (void *)base) == cudaSuccess) {
+    mine.off[0] = (long long)((uintptr_t)s0.phi[0] - (uintptr_t)base);
+    mine.off[1] = (long long)((uintptr_t)s0.phi[1] - (uintptr_t)base);
+    mine.nj = s0.gp.nj;
+    mine.ok = 1;
+  }
+  cudaGetLastError();  // (a failed IPC query is not sticky, but clear it)
+  const size_t n = (size_t)c.nranks;
+  char *d = nullptr;
+  CK(cudaMalloc(&d, (n + 1) * sizeof(PeerInfo)));
+  std::vector<PeerInfo> all(n);
+  CK(cudaMemcpyAsync(d + n * sizeof(PeerInfo), &mine, sizeof(PeerInfo), cudaMemcpyHostToDevice, c.stream));
+  NK(ncclAllGather(d + n * sizeof(PeerInfo), d, sizeof(PeerInfo), ncclChar, (ncclComm_t)c.nccl, c.stream));
+  CK(cudaMemcpyAsync(all.data(), d, n * sizeof(PeerInfo), cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  const int r = s0.rank;
+  int ok = 1;
+  for (int side = 0; side < 2 && ok; ++side) {
+    const int nb = side == 0 ? r - 1 : r + 1;
+    if (nb < 0 || nb >= c.nranks) continue;
+    void *p = nullptr;
+    if (!all[nb].ok || cudaIpcOpenMemHandle(&p, all[nb].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      ok = 0;
+      break;
+    }
+    c.peer_map[side] = p;
+    c.peer_phi[side][0] = (double *)((char *)p + all[nb].off[0]);
+    c.peer_phi[side][1] = (double *)((char *)p + all[nb].off[1]);
+    c.peer_nj[side] = all[nb].nj;
+  }
+  int *dok = reinterpret_cast<int *>(d);
+  CK(cudaMemcpyAsync(dok, &ok, sizeof(int), cudaMemcpyHostToDevice, c.stream));
+  NK(ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, (ncclComm_t)c.nccl, c.stream));
+  CK(cudaMemcpyAsync(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  cudaFree(d);
+  c.peer_halo = ok == 1;
+  if (!c.peer_halo)
+    for (int side = 0; side < 2; ++side) {
+      if (c.peer_map[side]) cudaIpcCloseMemHandle(c.peer_map[side]);
+      c.peer_map[side] = nullptr;
+      c.peer_phi[side][0] = c.peer_phi[side][1] = nullptr;
+    }
+  return IBM_OK;
+}
+
 int ibm_init(const ibm_config *cfg, void *d_workspace, size_t bytes, void *cuda_stream, ibm_ctx **out) {
   if (!out) return IBM_ERR_ARG;
   *out = nullptr;
@@ -995,6 +1140,12 @@ int ibm_init(const ibm_config *cfg, void *d_workspace, size_t bytes, void *cuda_
   c.comm = nullptr;
   c.ev_edge = c.ev_halo = nullptr;
   c.nccl_halo = nullptr;
+  c.peer_halo = false;
+  for (int q = 0; q < 2; ++q) {
+    c.peer_phi[q][0] = c.peer_phi[q][1] = nullptr;
+    c.peer_nj[q] = 0;
+    c.peer_map[q] = nullptr;
+  }
   auto fail = [&](int code) {
     fprintf(stderr, "ibm_init: %s\n", c.err.c_str());
     for (auto &e : c.ev)
@@ -1009,6 +1160,8 @@ int ibm_init(const ibm_config *cfg, void *d_workspace, size_t bytes, void *cuda_
     if (c.h_ctl) cudaFreeHost(c.h_ctl);
     if (c.h_red) cudaFreeHost(c.h_red);
     if (c.h_nan) cudaFreeHost(c.h_nan);
+    for (auto &p : c.peer_map)
+      if (p) cudaIpcCloseMemHandle(p);
     delete cp;
     return code;
   };
@@ -1106,6 +1259,13 @@ int ibm_init(const ibm_config *cfg, void *d_workspace, size_t bytes, void *cuda_
       return fail(IBM_ERR_NCCL);
     }
     c.nccl_halo = halo_comm;
+  }
+  {
+    const char *e = std::getenv("IBM_PEER_HALO");
+    const bool want = !(e && std::atoi(e) == 0);
+    if (c.loopback) c.peer_halo = want && c.sl.size() > 1;
+    else if (c.nranks > 1 && want && c.wf_m >= 2)
+      if (int st = open_peer_halo(c)) return fail(st);
   }
   c.body = Body{0, 0, 0, 0, 0, 0, 0};
   c.phi_cur = 0;
@@ -1296,6 +1456,7 @@ int ibm_query(const ibm_ctx *ctx, int key, int *out) {
     case IBM_QUERY_WF_L: *out = ctx->wf_L; return IBM_OK;
     case IBM_QUERY_SLABS: *out = (int)ctx->sl.size(); return IBM_OK;
     case IBM_QUERY_TB_M: *out = ctx->tb_m; return IBM_OK;
+    case IBM_QUERY_PEER_HALO: *out = ctx->peer_halo ? 1 : 0; return IBM_OK;
   }
   return IBM_ERR_ARG;
 }
@@ -1322,6 +1483,8 @@ int ibm_destroy(ibm_ctx *ctx) {
   cudaFreeHost(c.h_red);
   cudaFreeHost(c.h_nan);
   for (auto &kv : c.wf_segs) cudaFree(kv.second.second);
+  for (auto &p : c.peer_map)
+    if (p) cudaIpcCloseMemHandle(p);
   delete[] c.h_xn;
   delete[] c.h_yn;
   delete ctx;

@@ -116,6 +116,15 @@ struct WfArgs {
   unsigned long long *rho_bits;
   SorCtl *ctl;
   const WfSeg *seg;     // [segs] (wf_seg_table for this slab and L)
+  // Device-initiated halo: the pass also stores its output rows
+  // [0, peer_rows) at peer_lo + (row + kGhost) * pitch -- the top ghost rows of the
+  // slab below, in that slab's buffer for the next pass -- and rows [nj - peer_rows,
+  // nj) at peer_hi + (row + kGhost) * pitch -- the bottom ghost rows of the slab
+  // above (bases pre-offset by the host; nullptr: no such neighbour).  On one GPU
+  // (loopback slabs) the neighbours are plain device buffers; across processes they
+  // are CUDA-IPC mappings of the neighbours' buffers over NVLink.
+  double *peer_lo, *peer_hi;
+  int peer_rows;
 };
 constexpr int kWfMaxM = 4;  // fused iterations per pass: 2..kWfMaxM instantiated
 
@@ -200,6 +209,14 @@ struct Ctx {
   void *nccl_halo; // its split for the halo exchanges on the comm stream (overlapped with the pass)
   cudaStream_t comm;      // halo-exchange stream of the decomposed fused pass (nranks > 1 or loopback)
   cudaEvent_t ev_edge, ev_halo;  // edge items of a pass done / its output's halo rows exchanged
+  // Device-initiated halo of the fused Poisson pass (WfArgs::peer_*): on for
+  // loopback slabs, and across ranks when every rank mapped its neighbours' phi
+  // buffers by CUDA IPC at init (peer_phi[side][buffer], side 0 = rank - 1,
+  // 1 = rank + 1; peer_nj = their owned rows); IBM_PEER_HALO=0 turns it off.
+  bool peer_halo;
+  double *peer_phi[2][2];
+  int peer_nj[2];
+  void *peer_map[2];  // cudaIpcOpenMemHandle bases (closed in ibm_destroy)
   std::string err;
 };
 
@@ -214,6 +231,11 @@ bool sor_coop_fits(const SorArgs &a);
 cudaError_t launch_sor_coop(const SorArgs &a, int s0, cudaStream_t st);
 // TMA box of the SOR tile (x) and of its right-hand side (b)
 constexpr int kSorBoxW = 64, kSorBoxHx = 20, kSorBoxHb = 18;
+// 1-D box of the row coefficients cN, cS of a tile: the tile's SH = 20 rows from an
+// even start row (one row earlier when the tile's first row is odd), 22 rows.  A
+// TMA box must start 16-B aligned in its innermost dimension: an odd fp64 start
+// (slabs with an odd first global row) raised "illegal instruction".
+constexpr int kSorBoxRows1d = kSorBoxHx + 2;
 constexpr int kSorTileX = 60, kSorTileY = 16;
 void launch_sor_iteration(const SorArgs &a, cudaStream_t st, int grid);
 // temporally blocked Poisson pass: rows of the TMA box, segment length, launch

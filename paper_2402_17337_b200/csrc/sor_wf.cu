@@ -284,7 +284,7 @@ __device__ __forceinline__ void sfor(F &&f) {
 // Stage use: the chunk reads its two half-window stages SA, SB and, at step 0, the b row rb-1 from
 // the previous half's stage Sp; the hooks wait for the second half's stage and
 // refill a stage once it is no longer read (see wf_nstg).
-template <int WM, int LAG, int TP, int MODE, bool OWN, bool APX, class Hooks>
+template <int WM, int LAG, int TP, int MODE, bool OWN, bool APX, class Hooks, bool PEER = false>
 __device__ __forceinline__ void wf_chunk(double2 (&X)[NS][WfGeo<WM, LAG>::W], double2 (&B)[NS][WfGeo<WM, LAG>::W],
                                          const WfStage<WfGeo<WM, LAG>::CR> &SA, const WfStage<WfGeo<WM, LAG>::CR> &SB,
                                          const WfStage<WfGeo<WM, LAG>::CR> &Sp, const WfCols &C, const WfArgs &A,
@@ -337,6 +337,17 @@ __device__ __forceinline__ void wf_chunk(double2 (&X)[NS][WfGeo<WM, LAG>::W], do
       const bool pair_in = MODE == 2 || i0 + 2 * (l + 32 * st) + 1 < A.g.ni;
       st_pred(rowin && lane_own[st] && pair_in, ob + q * pitch + 64 * st, v);
       if (MODE < 2) st_pred1(rowin && lane_own[st] && !pair_in, ob + q * pitch + 64 * st, v.x);
+      if constexpr (PEER) {
+        // boundary rows also go straight into the neighbours' ghost rows (f3)
+        const long o = (long)(ro + kGhost) * pitch + (i0 + 2 * l) + 64 * st;
+        const bool lo = A.peer_lo != nullptr && ro >= 0 && ro < A.peer_rows;
+        const bool hi = A.peer_hi != nullptr && ro >= A.g.nj - A.peer_rows && ro < A.g.nj;
+        const bool ok = rowin && lane_own[st];
+        st_pred(ok && pair_in && lo, A.peer_lo + o, v);
+        st_pred1(ok && !pair_in && lo, A.peer_lo + o, v.x);
+        st_pred(ok && pair_in && hi, A.peer_hi + o, v);
+        st_pred1(ok && !pair_in && hi, A.peer_hi + o, v.x);
+      }
     }
     if constexpr (q == 0) hooks.after_first();  // the previous half's stage is no longer read
     if constexpr (q == CR) hooks.after_second();  // this window's first half: no longer read
@@ -504,7 +515,14 @@ __global__ void __launch_bounds__(32, (wf_min_blocks<WM, LAG>())) k_sor_wf(const
       } hooks{refill, bar, hA, G + hB};
       const WfStage<CR> &SA = st[(G + hA) % NSTG], &SB = st[(G + hB) % NSTG],
                         &Sp = st[(G + hA + NSTG - 1) % NSTG];
-      if (fast && interior && ownall)
+      // chunks storing slab boundary rows with a neighbour to feed: the predicated
+      // path with the peer stores (rows stored here: rb - DLO .. rb + W - 1 - DLO)
+      const bool peer = (A.peer_lo != nullptr && rb - DLO < A.peer_rows) ||
+                        (A.peer_hi != nullptr && rb + W - 1 - DLO >= g.nj - A.peer_rows);
+      if (peer)
+        wf_chunk<WM, LAG, TP, 0, false, APX, decltype(hooks) &, true>(X, B, SA, SB, Sp, C, A, rb, j0, j1, i0,
+                                                                     lane_own, hasf, cN0, cS0, tmax, hooks);
+      else if (fast && interior && ownall)
         wf_chunk<WM, LAG, TP, 2, true, APX>(X, B, SA, SB, Sp, C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax, hooks);
       else if (fast && interior)
         wf_chunk<WM, LAG, TP, 2, false, APX>(X, B, SA, SB, Sp, C, A, rb, j0, j1, i0, lane_own, hasf, cN0, cS0, tmax, hooks);

@@ -60,7 +60,7 @@ class ibm_step_stats(C.Structure):
 EXPORTS = ["ibm_workspace_size", "ibm_nccl_unique_id", "ibm_init", "ibm_set_body", "ibm_clear_body",
            "ibm_set_fields", "ibm_set_step", "ibm_step", "ibm_get_fields", "ibm_forces",
            "ibm_poisson_iterate", "ibm_query", "ibm_last_error", "ibm_destroy"]
-IBM_QUERY_WF_M, IBM_QUERY_WF_L, IBM_QUERY_SLABS, IBM_QUERY_TB_M = 0, 1, 2, 3
+IBM_QUERY_WF_M, IBM_QUERY_WF_L, IBM_QUERY_SLABS, IBM_QUERY_TB_M, IBM_QUERY_PEER_HALO = 0, 1, 2, 3, 4
 
 _lib = None
 
@@ -347,4 +347,5 @@ class Solver:
         """Launch configuration chosen by the library: "wf_m" (Poisson iterations per
         HBM pass), "wf_L" (fused-pass segment length, 0 before tuning), "slabs"."""
         return ibm_query(self.ctx, {"wf_m": IBM_QUERY_WF_M, "wf_L": IBM_QUERY_WF_L,
-                                    "slabs": IBM_QUERY_SLABS, "tb_m": IBM_QUERY_TB_M}[key])
+                                    "slabs": IBM_QUERY_SLABS, "tb_m": IBM_QUERY_TB_M,
+                                    "peer_halo": IBM_QUERY_PEER_HALO}[key])

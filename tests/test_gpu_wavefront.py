@@ -115,6 +115,34 @@ def test_loopback_slabs_fused(mods, wf_rows, m, P):
     assert_parity(o, g, ro, rg)
 
 
+@pytest.mark.parametrize("peer", ["1", "0"])
+@pytest.mark.parametrize("m", [2, 3, 4])
+@pytest.mark.parametrize("P,nx,ny", [(2, 128, 96), (3, 130, 98), (4, 257, 131)])
+def test_loopback_peer_halo(mods, wf_rows, monkeypatch, peer, m, P, nx, ny):
+    """Device-initiated halo: with IBM_PEER_HALO on, each slab's
+    fused pass stores its 2m boundary rows straight into the neighbours' ghost rows
+    (no exchange between passes); off, the rows go through the overlapped exchange.
+    Both bit-identical to the oracle, over ragged slabs and short segments."""
+    monkeypatch.setenv("IBM_PEER_HALO", peer)
+    wf_rows(10)
+    cfg = I.cfg1(nx=nx, ny=ny, steps=3, maxit_p=700)
+    o, g, ro, rg = run_pair(mods, cfg, cfg.steps, nranks=P, loopback=True, sor_batch=5, sor_fuse=m)
+    assert g.query("peer_halo") == int(peer)
+    assert_parity(o, g, ro, rg)
+
+
+@pytest.mark.parametrize("fuse", [1, 3])
+@pytest.mark.parametrize("P,ny", [(2, 50), (2, 53), (3, 98)])
+def test_loopback_odd_slab_rows(mods, wf_rows, fuse, P, ny):
+    """Slabs whose first global row is odd (colour template TP = 1): the one-
+    iteration pass loads its row coefficients by a 1-D TMA box, which must start
+    16-B aligned (an odd fp64 start raised "illegal instruction" before the fix)."""
+    wf_rows(0)
+    cfg = I.cfg1(nx=64, ny=ny, steps=2, maxit_p=500)
+    o, g, ro, rg = run_pair(mods, cfg, cfg.steps, nranks=P, loopback=True, sor_batch=5, sor_fuse=fuse)
+    assert_parity(o, g, ro, rg)
+
+
 @pytest.mark.parametrize("m", [3])
 def test_loopback_cylinder_fused(mods, wf_rows, m):
     """Body crossing a slab boundary (cylinder centred on the domain's mid row)."""

@@ -7,7 +7,9 @@ tier has one); the same decomposition runs on one GPU through the loopback
 transport (tests/test_gpu_wavefront.py, tests/test_gpu_parity.py).
 
 Cases: cfg1 (BJ configs[0]) at P = 2, 4, 8 (up to the device count) against the
-oracle, and the 16384^2 mesh (BJ configs[4]) with capped SOR solves at P = 2,
+oracle, with the fused pass's halo rows stored by the kernel into the neighbours'
+CUDA-IPC-mapped buffers (IBM_PEER_HALO=1) and through NCCL send/recv
+(IBM_PEER_HALO=0), and the 16384^2 mesh (BJ configs[4]) with capped SOR solves at P = 2,
 4, 8 against P = 1 -- on the fields' checksums and a sampled row set."""
 import os
 import socket
@@ -36,13 +38,14 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, case, q):
+def _worker(rank, world, port, case, q, peer="1"):
     import torch
     import torch.distributed as dist
 
     import paper_2402_17337_b200 as P
     from paper_2402_17337_b200.dist import bootstrap_nccl_id, slab_of
 
+    os.environ["IBM_PEER_HALO"] = peer  # device-initiated halo (CUDA-IPC peer stores) or NCCL send/recv
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(rank)
@@ -56,6 +59,7 @@ def _worker(rank, world, port, case, q):
         g.set_fields(*slab_of(u0, v0, p0, cfg.ny, world, rank))
         st, stats = g.step(steps)
         out = {n: g.get(n) for n in names}
+        out["peer_halo"] = g.query("peer_halo")
         rows = g.rows
         g.close()
         q.put((rank, st, stats, rows, out))
@@ -70,12 +74,12 @@ def _case(case):
     return cfg, 1, ("u", "v", "p")
 
 
-def _run(world, case):
+def _run(world, case, peer="1"):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q, peer)) for r in range(world)]
     for pr in procs:
         pr.start()
     res = sorted([q.get(timeout=1800) for _ in range(world)], key=lambda r: r[0])
@@ -83,6 +87,8 @@ def _run(world, case):
         pr.join(timeout=120)
         assert pr.exitcode == 0
     stats = res[0][2]
+    peers = {r[4].pop("peer_halo") for r in res}
+    assert peers == {int(peer)}, peers  # every rank on the same halo path (IPC mapping agreed)
     for r in res[1:]:
         assert r[1] == res[0][1]
         assert np.array_equal(r[2], stats)  # same iteration counts, residuals, forces on every rank
@@ -90,12 +96,13 @@ def _run(world, case):
     return res[0][1], stats, fields
 
 
+@pytest.mark.parametrize("peer", ["1", "0"])
 @pytest.mark.parametrize("world", [2, 4, 8])
-def test_nccl_slabs_cfg1_equal_oracle(oracle_mod, world):
+def test_nccl_slabs_cfg1_equal_oracle(oracle_mod, world, peer):
     if _ngpu() < world:
         pytest.skip("needs %d GPUs" % world)
     cfg, steps, names = _case("cfg1")
-    st, stats, fields = _run(world, "cfg1")
+    st, stats, fields = _run(world, "cfg1", peer)
     u0, v0, p0 = I.initial_fields(cfg.nx, cfg.ny, cfg.perturb)
     o = oracle_mod.Oracle(cfg.xn, cfg.yn, **cfg.solver_kwargs())
     o.set_body(*cfg.body_args())
