@@ -11,13 +11,13 @@ python bench.py > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err; c
 # launch list (cold-cache, serialised): the bench command with a short Poisson cap
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
     python bench.py --steps 1 --warmup 0 --maxit-p 200 --no-e2e --no-cpu-baseline --no-clocks --sor-batch 256 > /dev/null 2>&1
-# full captures: the fused Poisson pass (k_sor_wf, 2 iterations per launch) ~120 iterations into the
+# full captures: the fused Poisson pass (k_sor_wf, 3 iterations per launch) ~120 iterations into the
 # first step, the one-iteration pass (--sor-fuse 1) likewise, and the other kernels
 ncu --set full --clock-control none --import-source on -k regex:k_sor_wf -s 40 -c 1 -o gpurun_out/prof_wf_${TAG} -f \
     python bench.py --steps 1 --warmup 0 --maxit-p 220 --no-e2e --no-cpu-baseline --no-clocks --sor-batch 256 > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:'k_sor<.int.0' -s 40 -c 1 -o gpurun_out/prof_sor_${TAG} -f \
     python bench.py --steps 1 --warmup 0 --maxit-p 220 --no-e2e --no-cpu-baseline --no-clocks --sor-batch 256 --sor-fuse 1 > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:'k_pred|k_prhs|k_correct|k_classify|k_pflags|k_forces' -c 12 \
+ncu --set full --clock-control none --import-source on -k regex:'k_pred|k_prhs|k_correct|k_outlet|k_pext|k_forces' -c 12 \
     -o gpurun_out/prof_other_${TAG} -f python bench.py --steps 1 --warmup 0 --maxit-p 5 --maxit-uv 3 --no-e2e --no-cpu-baseline --no-clocks --sor-batch 256 > /dev/null 2>&1
 ncu --set full --clock-control none -k regex:k_sor -s 2 -c 1 -o gpurun_out/prof_uvsor_${TAG} -f \
     python bench.py --steps 1 --warmup 0 --maxit-p 5 --maxit-uv 10 --no-e2e --no-cpu-baseline --no-clocks --sor-batch 256 > /dev/null 2>&1

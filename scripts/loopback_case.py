@@ -1,3 +1,8 @@
+"""One loopback slab-decomposition case against the oracle, in its own process (a
+kernel fault cannot take other cases with it): prints OK / FAIL.
+Usage: python scripts/loopback_case.py PEER_HALO NRANKS NX NY M ROWS [SOR_FUSE]
+(PEER_HALO 0/1 -> IBM_PEER_HALO; ROWS -> IBM_WF_ROWS, 0 = the library's choice).
+Set IBM_DEBUG_SYNC=1 to locate a faulting kernel (a sync and check after each phase)."""
 import os, sys
 sys.path.insert(0, "/root/repo"); sys.path.insert(0, "/root/repo/tests")
 import ibm_inputs as I
