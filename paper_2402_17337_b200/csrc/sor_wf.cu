@@ -70,6 +70,16 @@ constexpr int WNT = 32;
 #define WF_LAG_DEFAULT 1
 #endif
 constexpr int SC = 64;  // stored columns per strip (lane l holds columns 2l, 2l+1)
+// Experiment knobs (build variants): WF_EARLYWAIT = 1 waits for both halves of a
+// window at its first step (one wait per chunk: the chunk body is one basic block
+// between the refills) instead of before its second half; WF_NSTG1 = stages per
+// warp at LAG 1 (their lead is NSTG1 - 1 halves minus what EARLYWAIT takes).
+#ifndef WF_EARLYWAIT
+#define WF_EARLYWAIT 0
+#endif
+#ifndef WF_NSTG1
+#define WF_NSTG1 4
+#endif
 template <int WM, int LAG>
 struct WfGeo {
   static constexpr int DLO = 1 + LAG * (2 * WM - 1);  // last half-sweep's row = entering row - DLO
@@ -83,7 +93,7 @@ struct WfGeo {
   // proxy fence (MEMBAR.ALL.CTA + FENCE.VIEW.ASYNC.S, which would also drain the
   // warp's stores) -- and NSTG-1 halves are in flight ahead of the one being
   // computed: 11 rows at LAG 1 (4 stages of 4 KB), 13 at LAG 2 (3 of 7 KB).
-  static constexpr int NSTG = LAG == 1 ? 4 : 3;
+  static constexpr int NSTG = LAG == 1 ? WF_NSTG1 : 3;
 };
 template <int CR>
 struct __align__(128) WfStage {  // half a window: CR rows of x and b
@@ -299,7 +309,7 @@ __device__ __forceinline__ void wf_chunk(double2 (&X)[NS][WfGeo<WM, LAG>::W], do
   double *const ob = A.xout + (long)(rb - DLO + kGhost) * pitch + (i0 + 2 * l);
   sfor<W>([&](auto qc) {
     constexpr int q = decltype(qc)::value;
-    if constexpr (q == CR) hooks.wait_second();  // second half's stage has landed
+    if constexpr (q == (WF_EARLYWAIT ? 0 : CR)) hooks.wait_second();  // second half's stage has landed
     // row rb+q enters the window; the b of row rb+q-1 (first needed in this step)
     // is read now rather than with its x one step earlier (one row less live)
     constexpr int qb = (q + W - 1) % W;
