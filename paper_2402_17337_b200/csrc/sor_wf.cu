@@ -294,14 +294,18 @@ __device__ __forceinline__ void sfor(F &&f) {
 // Stage use: the chunk reads its two half-window stages SA, SB and, at step 0, the b row rb-1 from
 // the previous half's stage Sp; the hooks wait for the second half's stage and
 // refill a stage once it is no longer read (see wf_nstg).
-template <int WM, int LAG, int TP, int MODE, bool OWN, bool APX, class Hooks, bool PEER = false>
+// H0, H1: the half-sweeps [H0, H1) this warp applies (all 2WM by default; the
+// two-warp pipeline k_sor_ws splits them).  SINK 0: the rows leaving the window go
+// to global memory; 1: to the next warp through hooks.emit (x and b of the row).
+template <int WM, int LAG, int TP, int MODE, bool OWN, bool APX, class Hooks, bool PEER = false, int H0 = 0,
+          int H1 = 2 * WM, int SINK = 0>
 __device__ __forceinline__ void wf_chunk(double2 (&X)[NS][WfGeo<WM, LAG>::W], double2 (&B)[NS][WfGeo<WM, LAG>::W],
                                          const WfStage<WfGeo<WM, LAG>::CR> &SA, const WfStage<WfGeo<WM, LAG>::CR> &SB,
                                          const WfStage<WfGeo<WM, LAG>::CR> &Sp, const WfCols &C, const WfArgs &A,
                                          int rb, int j0, int j1, int i0, const bool (&lane_own)[NS], bool hasf,
                                          double cN0, double cS0, unsigned long long (&tmax)[WM][NS], Hooks &&hooks) {
   using G = WfGeo<WM, LAG>;
-  constexpr int W = G::W, CR = G::CR, DLO = G::DLO;
+  constexpr int W = G::W, CR = G::CR, DLO = 1 + LAG * (H1 - H0 - 1);
   const int l = threadIdx.x & 31;
   const double omega = A.omega, omc = A.omc;
   const long pitch = A.g.pitch;
@@ -321,11 +325,11 @@ __device__ __forceinline__ void wf_chunk(double2 (&X)[NS][WfGeo<WM, LAG>::W], do
       X[st][q] = *reinterpret_cast<const double2 *>(&Sx.x[rx][2 * (l + 32 * st)]);
       B[st][qb] = *reinterpret_cast<const double2 *>(&Sb.b[rbb][2 * (l + 32 * st)]);
     }
-    sfor<2 * WM>([&](auto hc) {
-      constexpr int h = decltype(hc)::value;
-      constexpr int Q = ((q - 1 - LAG * h) % W + W) % W;  // slot of row rb + q - 1 - LAG h
-      constexpr int E = (TP + Q + h) & 1;                 // red (h even): (i + j) even
-      const int r = rb + q - 1 - LAG * h;
+    sfor<H1 - H0>([&](auto hc) {
+      constexpr int h = H0 + decltype(hc)::value;
+      constexpr int Q = ((q - 1 - LAG * (h - H0)) % W + W) % W;  // slot of row rb + q - 1 - LAG (h - H0)
+      constexpr int E = (TP + Q + h) & 1;                         // red (h even): (i + j) even
+      const int r = rb + q - 1 - LAG * (h - H0);
       [[maybe_unused]] const bool own = OWN || (r >= j0 && r < j1);
       // owned-row mask from the sign bits of r - j0 and j1 - 1 - r (no predicate)
       unsigned okm = 0xffffffffu;
@@ -341,6 +345,9 @@ __device__ __forceinline__ void wf_chunk(double2 (&X)[NS][WfGeo<WM, LAG>::W], do
     // row rb + q - DLO has received its last half-sweep: store the owned columns
     const int ro = rb + q - DLO;
     const bool rowin = OWN || (ro >= j0 && ro < j1);
+    if constexpr (SINK == 1) {
+      hooks.emit(q - DLO, X[0][((q - DLO) % W + W) % W], B[0][((q - DLO) % W + W) % W]);
+    } else {
 #pragma unroll
     for (int st = 0; st < NS; ++st) {
       const double2 v = X[st][((q - DLO) % W + W) % W];
@@ -358,6 +365,7 @@ __device__ __forceinline__ void wf_chunk(double2 (&X)[NS][WfGeo<WM, LAG>::W], do
         st_pred(ok && pair_in && hi, A.peer_hi + o, v);
         st_pred1(ok && !pair_in && hi, A.peer_hi + o, v.x);
       }
+    }
     }
     if constexpr (q == 0) hooks.after_first();  // the previous half's stage is no longer read
     if constexpr (q == CR) hooks.after_second();  // this window's first half: no longer read
@@ -563,6 +571,199 @@ __global__ void __launch_bounds__(32, (wf_min_blocks<WM, LAG>())) k_sor_wf(const
   }
 }
 
+// ============================================================================
+// Two-warp pipeline (IBM_WF_WS=1, experiment): one work item per CTA of two warps.
+// Warp A streams the strip from the TMA stages and applies half-sweeps 0 .. WM-1;
+// every row it has finished (x and its b) goes into a shared-memory ring of
+// half-window stages; warp B streams the ring and applies half-sweeps WM .. 2WM-1,
+// then stores.  Rows flow through A and then B in order, so every update sees the
+// operands of the one-warp pass (the oracle's).  Each warp carries half the
+// in-step dependency chain and about half the registers, so twice the warps are
+// resident.  Ring flow control: full[s] (32 arrivals of A's lanes after they wrote
+// the stage's 4 rows), empty[s] (32 arrivals of B's lanes after their last read).
+#ifndef WS_NSTG
+#define WS_NSTG 3
+#endif
+#ifndef WS_NR
+#define WS_NR 3
+#endif
+#ifndef WS_MINB
+#define WS_MINB 8
+#endif
+template <int WM>
+constexpr size_t ws_smem() {
+  using G = WfGeo<WM, 1>;
+  return (size_t)(WS_NSTG + WS_NR) * sizeof(WfStage<G::CR>) + (WS_NSTG + 2 * WS_NR) * sizeof(unsigned long long);
+}
+
+template <int WM, int TP, bool APX>
+__global__ void __launch_bounds__(64, WS_MINB) k_sor_ws(const __grid_constant__ WfArgs A) {
+  using Gm = WfGeo<WM, 1>;
+  constexpr int W = Gm::W, CR = Gm::CR, NSTG = WS_NSTG, NR = WS_NR, HA = WM;
+  constexpr unsigned kBytes = 2u * CR * SC * 8;
+  static_assert(CR == 4 && W == 8, "the ring assumes half windows of 4 rows");
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  const int l = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WfStage<CR> *st = reinterpret_cast<WfStage<CR> *>(smraw);
+  WfStage<CR> *ring = st + NSTG;
+  unsigned long long *tbar = reinterpret_cast<unsigned long long *>(ring + NR);
+  unsigned long long *full = tbar + NSTG, *empty = full + NR;
+  unsigned long long tmax[WM][NS];
+#pragma unroll
+  for (int i = 0; i < WM; ++i) tmax[i][0] = 0ull;
+  const int item = blockIdx.x;
+  const WfItem it = wf_item<WM, 1>(A, item);
+  const Geo &g = A.g;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSTG; ++s) mbar_init(&tbar[s], 1);
+    for (int s = 0; s < NR; ++s) {
+      mbar_init(&full[s], 32);
+      mbar_init(&empty[s], 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 0)
+    for (int hc = 0; hc < NSTG - 1 && hc < 2 * it.nch; ++hc)
+      tma_load_pair_elect(&tbar[hc], kBytes, &st[hc].x[0][0], &A.tmx, &st[hc].b[0][0], &A.tmb, it.i0,
+                          it.rs + hc * CR + kGhost);
+  if (*(volatile int *)&A.ctl->k_done >= 0) {  // converged earlier: drain the loads in flight
+    if (warp == 0)
+      for (int hc = 0; hc < NSTG - 1 && hc < 2 * it.nch; ++hc) mbar_wait_warp(&tbar[hc], 0);
+    return;
+  }
+  const int i0 = it.i0, j0 = it.j0, j1 = it.j1, rs = it.rs, nch = it.nch;
+  bool lane_own[NS];
+  lane_own[0] = l >= WM && l <= 31 - WM && i0 + 2 * l < g.ni;
+  const bool interior = i0 >= A.ui0 && i0 + SC <= A.ui1;
+  const bool boxstrip = !A.box.empty() && i0 < A.box.i1 && i0 + SC > A.box.i0;
+  const WfSeg sg = A.seg[it.sy];
+  const double cN0 = sg.cN0, cS0 = sg.cS0;
+  // rows this warp updates in a chunk at base rb: rb - DLO .. rb + W - 2
+  const int DLO = warp == 0 ? HA : 2 * WM - HA;
+  int irr0 = sg.irr0, irr1 = sg.irr1;
+  if (boxstrip) {
+    const int lo = max(A.box.j0, rs - 2 * WM), hi = min(A.box.j1 - 1, rs + nch * W - 2);
+    if (lo <= hi) {
+      irr0 = min(irr0, lo);
+      irr1 = max(irr1, hi);
+    }
+  }
+  WfCols C;
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int gi = i0 + 2 * l + e;
+    const bool in = gi >= 0 && gi < g.ni;
+    const double cE = in ? A.cE[gi] : 0.0, cW = in ? A.cW[gi] : 0.0;
+    C.cD[0][e] = in ? A.cD[gi] : 0.0;
+    C.aE[0][e] = cE;
+    C.aW[0][e] = cW;
+    C.sEW[0][e] = cE + cW;
+    C.yu[0][e] = __drcp_rn((C.sEW[0][e] + (cN0 + cS0)) + C.cD[0][e]);
+    C.inm[0][e] = (gi >= A.ui0 && gi < A.ui1) ? 0xffffffffu : 0u;
+  }
+  double2 X[NS][W], B[NS][W];
+#pragma unroll
+  for (int q = 0; q < W; ++q) X[0][q] = B[0][q] = make_double2(0.0, 0.0);
+  for (int c = 0; c < nch; ++c) {
+    const int hA = 2 * c, hB = hA + 1;
+    const int rb = rs + c * W;
+    const bool fast = rb + W - 2 < irr0 || rb - DLO > irr1;
+    const bool hasf = boxstrip && rb + W - 2 >= A.box.j0 && rb - DLO < A.box.j1;
+    const bool ownall = rb - DLO >= j0 && rb + W - 2 < j1;
+    if (warp == 0) {
+      // ---- warp A: TMA stages in, half-sweeps 0 .. HA-1, finished rows into the ring
+      mbar_wait_warp(&tbar[hA % NSTG], (hA / NSTG) & 1);
+      auto refill = [&](int h) {
+        __syncwarp();
+        const int hn = h + NSTG - 1, sr = hn % NSTG;
+        tma_load_pair_elect_if(hn < 2 * nch, &tbar[sr], kBytes, &st[sr].x[0][0], &A.tmx, &st[sr].b[0][0], &A.tmb,
+                               i0, rs + hn * CR + kGhost);
+      };
+      struct HooksA {
+        decltype(refill) &rf;
+        unsigned long long *tbar, *full, *empty;
+        WfStage<CR> *ring;
+        int hA, c, l;
+        __device__ __forceinline__ void after_first() { rf(hA); }
+        __device__ __forceinline__ void wait_second() {
+          mbar_wait_warp(&tbar[(hA + 1) % NSTG], ((hA + 1) / NSTG) & 1);
+        }
+        __device__ void after_second() { rf(hA + 1); }
+        // row rb + D (D = q - HA, a constant after inlining) leaves A: ring half
+        // 2c + floor(D / 4), position D mod 4
+        __device__ __forceinline__ void emit(int D, double2 vx, double2 vb) {
+          const int P = ((D % 4) + 4) % 4, KO = D >= 0 ? D / 4 : -1;
+          const int kh = 2 * c + KO;
+          if (kh < 0) return;  // (rows before the stream: nothing to hand over)
+          const int s = kh % NR;
+          if (P == 0 && kh >= NR) mbar_wait_warp(&empty[s], ((kh / NR) - 1) & 1);
+          *reinterpret_cast<double2 *>(&ring[s].x[P][2 * l]) = vx;
+          *reinterpret_cast<double2 *>(&ring[s].b[P][2 * l]) = vb;
+          if (P == 3) mbar_arrive(&full[s]);
+        }
+      } hooks{refill, tbar, full, empty, ring, hA, c, l};
+      const WfStage<CR> &SA = st[hA % NSTG], &SB = st[hB % NSTG], &Sp = st[(hA + NSTG - 1) % NSTG];
+      if (fast && interior && ownall)
+        wf_chunk<WM, 1, TP, 2, true, APX, HooksA &, false, 0, HA, 1>(X, B, SA, SB, Sp, C, A, rb, j0, j1, i0, lane_own,
+                                                                    hasf, cN0, cS0, tmax, hooks);
+      else if (fast && interior)
+        wf_chunk<WM, 1, TP, 2, false, APX, HooksA &, false, 0, HA, 1>(X, B, SA, SB, Sp, C, A, rb, j0, j1, i0,
+                                                                     lane_own, hasf, cN0, cS0, tmax, hooks);
+      else if (fast)
+        wf_chunk<WM, 1, TP, 1, false, APX, HooksA &, false, 0, HA, 1>(X, B, SA, SB, Sp, C, A, rb, j0, j1, i0,
+                                                                     lane_own, hasf, cN0, cS0, tmax, hooks);
+      else
+        wf_chunk<WM, 1, TP, 0, false, APX, HooksA &, false, 0, HA, 1>(X, B, SA, SB, Sp, C, A, rb, j0, j1, i0,
+                                                                     lane_own, hasf, cN0, cS0, tmax, hooks);
+    } else {
+      // ---- warp B: ring in, half-sweeps HA .. 2WM-1, rows out to global memory
+      mbar_wait_warp(&full[hA % NR], (hA / NR) & 1);
+      struct HooksB {
+        unsigned long long *full, *empty;
+        int hA;
+        __device__ void after_first() {  // the previous half's ring stage is no longer read
+          __syncwarp();
+          if (hA > 0) mbar_arrive(&empty[(hA - 1) % NR]);
+        }
+        __device__ void wait_second() { mbar_wait_warp(&full[(hA + 1) % NR], ((hA + 1) / NR) & 1); }
+        __device__ void after_second() {
+          __syncwarp();
+          mbar_arrive(&empty[hA % NR]);
+        }
+        __device__ void emit(int, double2, double2) {}
+      } hooks{full, empty, hA};
+      const WfStage<CR> &SA = ring[hA % NR], &SB = ring[hB % NR], &Sp = ring[(hA + NR - 1) % NR];
+      if (fast && interior && ownall)
+        wf_chunk<WM, 1, TP, 2, true, APX, HooksB &, false, HA, 2 * WM, 0>(X, B, SA, SB, Sp, C, A, rb, j0, j1, i0,
+                                                                          lane_own, hasf, cN0, cS0, tmax, hooks);
+      else if (fast && interior)
+        wf_chunk<WM, 1, TP, 2, false, APX, HooksB &, false, HA, 2 * WM, 0>(X, B, SA, SB, Sp, C, A, rb, j0, j1, i0,
+                                                                           lane_own, hasf, cN0, cS0, tmax, hooks);
+      else if (fast)
+        wf_chunk<WM, 1, TP, 1, false, APX, HooksB &, false, HA, 2 * WM, 0>(X, B, SA, SB, Sp, C, A, rb, j0, j1, i0,
+                                                                           lane_own, hasf, cN0, cS0, tmax, hooks);
+      else
+        wf_chunk<WM, 1, TP, 0, false, APX, HooksB &, false, HA, 2 * WM, 0>(X, B, SA, SB, Sp, C, A, rb, j0, j1, i0,
+                                                                           lane_own, hasf, cN0, cS0, tmax, hooks);
+    }
+  }
+  // A: the last half it partly filled is complete as far as B needs it (the rows it
+  // did not write lie past every stored row's dependency cone)
+  if (warp == 0) {
+    __syncwarp();
+    mbar_arrive(&full[(2 * nch - 1) % NR]);
+  }
+#pragma unroll
+  for (int i = 0; i < WM; ++i) {
+    unsigned long long t = 0ull;
+    if (l >= WM && l <= 31 - WM) t = wf_res_word<APX>(tmax[i][0]);
+#pragma unroll
+    for (int off = 16; off; off >>= 1) t = umax64(t, __shfl_xor_sync(FULL, t, off));
+    if (l == 0 && t) atomicMax(&A.rho_bits[A.k + i], APX ? t << 32 : t);
+  }
+}
+
 template <int WM, int LAG, int TP, bool APX>
 int wf_blocks_per_sm() {
   static int per = 0;
@@ -591,8 +792,33 @@ static bool wf_persist() {
   }();
   return p;
 }
+static bool wf_ws() {
+  static const bool p = [] {
+    const char *e = std::getenv("IBM_WF_WS");
+    return e && std::atoi(e) == 1;
+  }();
+  return p;
+}
+template <int WM, int TP, bool APX>
+void ws_launch(const WfArgs &a, cudaStream_t s) {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(k_sor_ws<WM, TP, APX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ws_smem<WM>());
+    done = true;
+  }
+  k_sor_ws<WM, TP, APX><<<a.items, 64, ws_smem<WM>(), s>>>(a);
+}
 template <int WM, int LAG, bool APX>
 void wf_launch_tp(const WfArgs &a, cudaStream_t s) {
+  if constexpr (LAG == 1 && WM == 3) {
+    if (wf_ws() && !a.peer_lo && !a.peer_hi) {
+      if (a.g.gj0 & 1)
+        ws_launch<WM, 1, APX>(a, s);
+      else
+        ws_launch<WM, 0, APX>(a, s);
+      return;
+    }
+  }
   if (a.g.gj0 & 1) {
     const int grid = wf_persist() ? std::min(a.items, wf_blocks_per_sm<WM, LAG, 1, APX>() * sm_count()) : a.items;
     wf_blocks_per_sm<WM, LAG, 1, APX>();
