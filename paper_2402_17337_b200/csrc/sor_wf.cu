@@ -19,13 +19,15 @@
 // recomputed by the neighbouring items and are never stored nor counted, so
 // every stored value and every residual term is bit-identical to the oracle's.
 //
-// Rows arrive by TMA in chunks of W rows (x and b, 64 x W boxes; the TMA unit
-// zero-fills outside the array, the oracle's "0 outside the family") into a
-// per-warp double-buffered stage armed on an mbarrier.  Chunks whose rows are
-// all inside the family, away from the body box and carry the segment's
-// reference row coefficients take a check-free path with per-column
-// reciprocals; the rest (domain edges, body, stretched rows) the predicated one.
-// One warp per CTA (one work item), 8 per SM.
+// Rows arrive by TMA in half windows of W/2 rows (x and b, 64 x W/2 boxes; the
+// TMA unit zero-fills outside the array, the oracle's "0 outside the family")
+// into a per-warp ring of stages armed on mbarriers, issued by an elected lane.
+// Chunks whose rows are all inside the family, away from the body box and carry
+// the segment's reference row coefficients (host-built WfSeg table) take a
+// check-free path with per-column reciprocals; the rest (domain edges, body,
+// stretched rows) the predicated one.  One warp per CTA (one work item), 8 per SM.
+// Decomposed grids: chunks that store a slab's boundary rows also store them
+// into the neighbours' ghost rows (WfArgs::peer_*, device-initiated halo).
 //
 // Residual (APX): the max of the high word of |d|, a lower bound of rho whose
 // stops are provisional and confirmed by the host's exact replay of the pass
@@ -293,7 +295,7 @@ __device__ __forceinline__ void sfor(F &&f) {
 // the instruction cache.)
 // Stage use: the chunk reads its two half-window stages SA, SB and, at step 0, the b row rb-1 from
 // the previous half's stage Sp; the hooks wait for the second half's stage and
-// refill a stage once it is no longer read (see wf_nstg).
+// refill a stage once it is no longer read (see WfGeo::NSTG).
 // H0, H1: the half-sweeps [H0, H1) this warp applies (all 2WM by default; the
 // two-warp pipeline k_sor_ws splits them).  SINK 0: the rows leaving the window go
 // to global memory; 1: to the next warp through hooks.emit (x and b of the row).
@@ -513,7 +515,7 @@ __global__ void __launch_bounds__(32, (wf_min_blocks<WM, LAG>())) k_sor_wf(const
       const bool ownall = rb - DLO >= j0 && rb + W - 2 < j1;
       // refill the stage of half h - 1 with half h + 3 -- of this item, or of the
       // next one near the end of this one -- once the first step of half h has read
-      // its last b row (see wf_nstg)
+      // its last b row (see WfGeo::NSTG)
       auto refill = [&](int h) {
         __syncwarp();
         const int hn = h + NSTG - 1, sr = (G + hn) % NSTG;
