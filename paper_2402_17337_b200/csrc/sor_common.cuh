@@ -63,6 +63,20 @@ __device__ __forceinline__ void mbar_wait_warp(unsigned long long *bar, uint32_t
     if (__all_sync(0xffffffffu, done)) break;
   }
 }
+// the same with a watchdog: traps (the launch fails) instead of spinning forever
+// when the phase never completes -- for the experimental producer / consumer rings
+__device__ __forceinline__ void mbar_wait_warp_bounded(unsigned long long *bar, uint32_t phase) {
+  for (unsigned n = 0;; ++n) {
+    uint32_t done;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    if (__all_sync(0xffffffffu, done)) break;
+    if (n > (1u << 24)) __trap();
+  }
+}
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1,
                                             unsigned long long *bar) {
   asm volatile(

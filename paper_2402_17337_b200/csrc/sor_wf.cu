@@ -699,7 +699,7 @@ __global__ void __launch_bounds__(64, WS_MINB) k_sor_ws(const __grid_constant__ 
           const int kh = 2 * c + KO;
           if (kh < 0) return;  // (rows before the stream: nothing to hand over)
           const int s = kh % NR;
-          if (P == 0 && kh >= NR) mbar_wait_warp(&empty[s], ((kh / NR) - 1) & 1);
+          if (P == 0 && kh >= NR) mbar_wait_warp_bounded(&empty[s], ((kh / NR) - 1) & 1);
           *reinterpret_cast<double2 *>(&ring[s].x[P][2 * l]) = vx;
           *reinterpret_cast<double2 *>(&ring[s].b[P][2 * l]) = vb;
           if (P == 3) mbar_arrive(&full[s]);
@@ -720,7 +720,7 @@ __global__ void __launch_bounds__(64, WS_MINB) k_sor_ws(const __grid_constant__ 
                                                                      lane_own, hasf, cN0, cS0, tmax, hooks);
     } else {
       // ---- warp B: ring in, half-sweeps HA .. 2WM-1, rows out to global memory
-      mbar_wait_warp(&full[hA % NR], (hA / NR) & 1);
+      mbar_wait_warp_bounded(&full[hA % NR], (hA / NR) & 1);
       struct HooksB {
         unsigned long long *full, *empty;
         int hA;
@@ -728,7 +728,7 @@ __global__ void __launch_bounds__(64, WS_MINB) k_sor_ws(const __grid_constant__ 
           __syncwarp();
           if (hA > 0) mbar_arrive(&empty[(hA - 1) % NR]);
         }
-        __device__ void wait_second() { mbar_wait_warp(&full[(hA + 1) % NR], ((hA + 1) / NR) & 1); }
+        __device__ void wait_second() { mbar_wait_warp_bounded(&full[(hA + 1) % NR], ((hA + 1) / NR) & 1); }
         __device__ void after_second() {
           __syncwarp();
           mbar_arrive(&empty[hA % NR]);
