@@ -22,6 +22,9 @@ ap.add_argument("--maxit-p", type=int, default=100000)
 ap.add_argument("--tol-p", type=float, default=1e-6)
 ap.add_argument("--max-minutes", type=float, default=150.0)
 ap.add_argument("--out-prefix", default="gpurun_out/f1")
+ap.add_argument("--ckpt", default=None, help="checkpoint file: resumed from if present, rewritten at the end "
+                "(u, v, p, phi, C^{n-1} and the step counter: a bit-exact continuation, test_checkpoint_restore)")
+ap.add_argument("--history", default=None, help="CSV of the steps before the checkpoint (prepended to the summary)")
 a = ap.parse_args()
 cfg = I.cfg3(level=a.level, omega_p=a.omega_p, maxit_p=a.maxit_p, tol_p=a.tol_p)
 body = cfg.body_args()
@@ -31,13 +34,29 @@ steps_per_cycle = int(round(period / cfg.dt))
 total = int(round(a.cycles * steps_per_cycle))
 g = P.Solver(cfg.xn, cfg.yn, **cfg.solver_kwargs())
 g.set_body(*body)
-g.set_fields(*I.initial_fields(cfg.nx, cfg.ny))
+hist, status_counts, done, diverged = [], {}, 0, False
+if a.ckpt and os.path.exists(a.ckpt):
+    import paper_2402_17337_b200.ibm as M
+    z = np.load(a.ckpt)
+    g.set_fields(z["u"], z["v"], z["p"], phi=z["phi"], restart=False)
+    cu, cv = np.ascontiguousarray(z["cu_prev"]), np.ascontiguousarray(z["cv_prev"])
+    M.ibm_set_fields(g.ctx, (1 << 10) | (1 << 11), {10: cu.ctypes.data, 11: cv.ctypes.data}, M.IBM_HOST)
+    done = int(z["step"])
+    g.set_step(done, True)
+    print("resumed at step", done, flush=True)
+else:
+    g.set_fields(*I.initial_fields(cfg.nx, cfg.ny))
+if a.history and os.path.exists(a.history):
+    prev = np.genfromtxt(a.history, delimiter=",", skip_header=1)
+    prev = prev[prev[:, 0] <= done]
+    hist = [list(r) for r in prev]
 os.makedirs(os.path.dirname(a.out_prefix) or ".", exist_ok=True)
 fcsv = open(a.out_prefix + ".csv", "w", newline="")
 w = csv.writer(fcsv)
 w.writerow(["step", "t_bar", "cd", "cl", "it_uv", "it_p", "rho_p", "status", "ms_step"])
+for r in hist:
+    w.writerow(r)
 t0 = time.time()
-hist, status_counts, done, diverged = [], {}, 0, False
 while done < total and (time.time() - t0) < 60 * a.max_minutes:
     n = min(a.chunk, total - done)
     st, S = g.step(n)
@@ -54,6 +73,9 @@ while done < total and (time.time() - t0) < 60 * a.max_minutes:
     if st == 3 or not np.all(np.isfinite(S[:, 5:7])):
         diverged = True
         break
+if a.ckpt and not diverged:
+    snap = {n: g.get(n) for n in ("u", "v", "p", "phi", "cu_prev", "cv_prev")}
+    np.savez(a.ckpt, step=done, **snap)
 H = np.array(hist, dtype=float)
 summ = {"config": cfg.describe(), "tb_m": g.query("tb_m"), "steps_done": done, "steps_target": total,
         "steps_per_cycle": steps_per_cycle, "diverged": diverged, "wall_s": time.time() - t0,
