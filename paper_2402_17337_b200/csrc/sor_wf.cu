@@ -682,29 +682,45 @@ __global__ void __launch_bounds__(64, WS_MINB) k_sor_ws(const __grid_constant__ 
         tma_load_pair_elect_if(hn < 2 * nch, &tbar[sr], kBytes, &st[sr].x[0][0], &A.tmx, &st[sr].b[0][0], &A.tmb,
                                i0, rs + hn * CR + kGhost);
       };
+      // ring stages of the halves this chunk emits into: 2c-1 (tail), 2c, 2c+1 (head)
       struct HooksA {
-        decltype(refill) &rf;
+        decltype(refill) *rf;
         unsigned long long *tbar, *full, *empty;
-        WfStage<CR> *ring;
-        int hA, c, l;
-        __device__ __forceinline__ void after_first() { rf(hA); }
+        double *rl;     // this lane's element of ring stage 0, row 0 (x)
+        int sidx[3];    // ring stages of the halves this chunk emits into: 2c-1 (tail), 2c, 2c+1 (head)
+        int hA, c, ewait1, ewait2;  // parities of the empty waits due for halves 2c, 2c+1 (< 0: none)
+        __device__ __forceinline__ void after_first() { (*rf)(hA); }
         __device__ __forceinline__ void wait_second() {
           mbar_wait_warp(&tbar[(hA + 1) % NSTG], ((hA + 1) / NSTG) & 1);
         }
-        __device__ void after_second() { rf(hA + 1); }
+        __device__ __forceinline__ void after_second() { (*rf)(hA + 1); }
         // row rb + D (D = q - HA, a constant after inlining) leaves A: ring half
         // 2c + floor(D / 4), position D mod 4
         __device__ __forceinline__ void emit(int D, double2 vx, double2 vb) {
+          constexpr int kStage = (int)(sizeof(WfStage<CR>) / sizeof(double)), kB = CR * SC;
           const int P = ((D % 4) + 4) % 4, KO = D >= 0 ? D / 4 : -1;
-          const int kh = 2 * c + KO;
-          if (kh < 0) return;  // (rows before the stream: nothing to hand over)
-          const int s = kh % NR;
-          if (P == 0 && kh >= NR) mbar_wait_warp_bounded(&empty[s], ((kh / NR) - 1) & 1);
-          *reinterpret_cast<double2 *>(&ring[s].x[P][2 * l]) = vx;
-          *reinterpret_cast<double2 *>(&ring[s].b[P][2 * l]) = vb;
-          if (P == 3) mbar_arrive(&full[s]);
+          if (KO < 0 && c == 0) return;  // (rows before the stream: nothing to hand over)
+          const int si = sidx[KO + 1];
+          if (P == 0 && KO == 0 && ewait1 >= 0) mbar_wait_warp_bounded(&empty[si], ewait1 & 1);
+          if (P == 0 && KO == 1 && ewait2 >= 0) mbar_wait_warp_bounded(&empty[si], ewait2 & 1);
+          double *px = rl + si * kStage + P * SC;
+          *reinterpret_cast<double2 *>(px) = vx;
+          *reinterpret_cast<double2 *>(px + kB) = vb;
+          if (P == 3) mbar_arrive(&full[si]);
         }
-      } hooks{refill, tbar, full, empty, ring, hA, c, l};
+      } hooks;
+      hooks.rf = &refill;
+      hooks.tbar = tbar;
+      hooks.full = full;
+      hooks.empty = empty;
+      hooks.rl = &ring[0].x[0][2 * l];
+      hooks.hA = hA;
+      hooks.c = c;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) hooks.sidx[k] = max(2 * c - 1 + k, 0) % NR;
+      // (use u = kh / NR of a stage needs B's release of use u - 1: parity (u - 1) & 1)
+      hooks.ewait1 = 2 * c >= NR ? (2 * c) / NR - 1 : -1;
+      hooks.ewait2 = 2 * c + 1 >= NR ? (2 * c + 1) / NR - 1 : -1;
       const WfStage<CR> &SA = st[hA % NSTG], &SB = st[hB % NSTG], &Sp = st[(hA + NSTG - 1) % NSTG];
       if (fast && interior && ownall)
         wf_chunk<WM, 1, TP, 2, true, APX, HooksA &, false, 0, HA, 1>(X, B, SA, SB, Sp, C, A, rb, j0, j1, i0, lane_own,
