@@ -364,7 +364,11 @@ def main():
                        "tol_p": cfg.tol_p, "maxit_p": cfg.maxit_p, "omega_uv": cfg.omega_uv,
                        "tol_uv": cfg.tol_uv, "maxit_uv": cfg.maxit_uv, "body": "foil a=0.5 b=0.06 h=0.16 k=2pi",
                        "l2": "inputs larger than L2 (%.1f GB workspace, 126 MB L2)" % (g.ws.numel() / 1e9),
-                       "parallelism": "slab%d" % world},
+                       "parallelism": "slab%d" % world,
+                       "note": ("every Poisson solve stops at maxit_p (omega_p %.2f does not reach tol_p at this size): "
+                                "ms_per_step is the time of a capped step, a throughput figure, not a converged "
+                                "physical time step" % cfg.omega_p) if float(stats[:, 2].min()) >= cfg.maxit_p else
+                               "Poisson solves converged"},
             "it_p": stats[:, 2].tolist(), "it_uv": stats[:, 1].tolist(),
             "poisson_ms_per_iteration": 1e3 * avg_iter_s, "poisson_ms_per_pass": 1e3 * avg_launch_s,
             "sor_fuse": fuse, "uv_sor_ms": uvsor_ms / args.steps,
