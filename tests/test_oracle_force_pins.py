@@ -331,3 +331,26 @@ def test_oracle_omp_bitwise_equal_seq(oracle_mod, case):
     assert np.array_equal(t0, t1)
     for k in f0:
         assert np.array_equal(f0[k], f1[k]), k
+
+
+@pytest.mark.parametrize("threads", ["2", "4"])
+def test_oracle_omp_bitwise_equals_seq(oracle_mod, monkeypatch, threads):
+    """oracle_omp (the same C source with -fopenmp, the all-core CPU baseline of
+    bench.py and the SOL1 analogue of the performance report) must give the
+    one-thread oracle's fields and statistics bit for bit: its loops split rows of
+    one colour / one kernel, and the only sums on the step path (forces) stay
+    serial.  BJ configs[0] with the body, 4 steps (converged and capped solves)."""
+    monkeypatch.setenv("OMP_NUM_THREADS", threads)
+    cfg = I.cfg1(steps=4, maxit_p=600)
+    u0, v0, p0 = I.initial_fields(cfg.nx, cfg.ny, cfg.perturb)
+    out = []
+    for omp in (False, True):
+        o = oracle_mod.Oracle(cfg.xn, cfg.yn, omp=omp, **cfg.solver_kwargs())
+        o.set_body(*cfg.body_args())
+        o.set_fields(u0, v0, p0)
+        st, stats = o.step(cfg.steps)
+        out.append((st, stats, {n: o.get(n) for n in ("u", "v", "p", "phi", "fu", "fv", "q")}))
+    assert out[0][0] == out[1][0]
+    assert np.array_equal(out[0][1], out[1][1])
+    for n in out[0][2]:
+        assert np.array_equal(out[0][2][n], out[1][2][n]), n
