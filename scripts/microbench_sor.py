@@ -34,4 +34,21 @@ for iters in (10, 200):
     res[iters] = {"ms_per_it": ms / iters, "host_ms_per_it": 1e3 * (t1 - t0) / iters,
                   "GBs": 24 * cfg.nx * cfg.ny / (ms / iters / 1e3) / 1e9,
                   "pass_GBs": 24 * cfg.nx * cfg.ny / (ms / iters * m / 1e3) / 1e9}
+# SURVEY §8(d) cfg4(i) protocol: tolerance off, 20 warm-up iterations, then 5 repetitions of 200
+# iterations, median (MICROBENCH_REPS=0 skips it)
+reps = int(os.environ.get("MICROBENCH_REPS", "5"))
+if reps:
+    g.poisson_iterate(20)
+    times = []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(g.stream)
+        g.poisson_iterate(200)
+        e1.record(g.stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) / 200)
+    med = float(np.median(times))
+    res["protocol_8d"] = {"ms_per_it_median": med, "ms_per_it_all": times, "ms_per_pass": med * m,
+                          "pass_GBs": 24 * cfg.nx * cfg.ny / (med * m / 1e3) / 1e9}
 print(json.dumps(res))
